@@ -1,0 +1,32 @@
+# Build the sm_100a C-ABI library and the CPU oracle.
+#   make -j8            # both
+#   make lib / oracle
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
+           -Iinclude -Ipaper_2008_12336_b200/csrc --expt-relaxed-constexpr
+PKG := paper_2008_12336_b200
+SRC := $(wildcard $(PKG)/csrc/*.cu)
+OBJ := $(patsubst $(PKG)/csrc/%.cu,build/obj/%.o,$(SRC))
+HDR := $(wildcard $(PKG)/csrc/*.cuh) include/gosh_b200.h
+LIB := $(PKG)/libgosh_b200.so
+
+all: lib oracle
+
+lib: $(LIB)
+
+build/obj/%.o: $(PKG)/csrc/%.cu $(HDR)
+	@mkdir -p build/obj
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIB): $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -cudart static
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -C oracle clean
+
+.PHONY: all lib oracle clean

@@ -1,0 +1,182 @@
+/*
+ * gosh_b200.h -- C ABI of the B200-native GOSH multilevel-embedding path.
+ *
+ * This is the drop-in boundary.  The reference (mlembed, Python + numba) has
+ * no FFI; its operator boundary is the set of numba kernels that take raw
+ * numpy arrays and mutate them in place.  Every entry point below replaces
+ * one of those kernels (cited file:line under /root/reference/pkg/src/mlembed)
+ * and keeps its argument meaning.  Differences forced by the device:
+ *
+ *   - all array arguments are DEVICE pointers (CUDA global memory), plain
+ *     C types only; the caller owns every buffer;
+ *   - work that needs scratch space takes a caller-provided workspace whose
+ *     size is reported by the matching *_workspace() query;
+ *   - every call is asynchronous on `stream` (a cudaStream_t passed as void*),
+ *     except the ones documented as "synchronizes" (they return a count that
+ *     sizes the caller's next allocation);
+ *   - every call returns GB_OK (0) or a negative GB_E* code; gb_last_error()
+ *     returns a thread-local message for the most recent failure.
+ *
+ * Host binding used by the package: ctypes (paper_2008_12336_b200/_lib.py).
+ */
+#ifndef GOSH_B200_H
+#define GOSH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GB_OK 0
+#define GB_E_INVALID (-1)   /* bad argument (maps to ValueError)          */
+#define GB_E_CUDA (-2)      /* CUDA runtime error (maps to RuntimeError)  */
+#define GB_E_WORKSPACE (-3) /* workspace too small                        */
+#define GB_E_UNSUPPORTED (-4)
+
+/* train flags */
+#define GB_TRAIN_REUSE 1u  /* TrainConfig.reuse_updated_source (trainer.py:47-50) */
+#define GB_TRAIN_EXACT 2u  /* one source group, reference order, serial fp64 dot  */
+
+/* csr build flags */
+#define GB_CSR_DROP_SELF 1u  /* from_edges drops self-loops (graph.py:127-128)  */
+#define GB_CSR_SYMMETRIZE 2u /* undirected: add reversed arcs (graph.py:129-130) */
+
+/* status block written by the training kernels (device memory, 4 x int64):
+ *   [0] non-finite flag (0/1)            -- fused replacement of the
+ *   [1] first epoch that saw a non-finite    isfinite scan, trainer.py:236-237
+ *   [2] positive updates applied (pool kernels; train_pair return value)
+ *   [3] reserved                                                              */
+#define GB_STATUS_WORDS 4
+
+const char *gb_last_error(void);
+int gb_version(void);
+/* Device properties the host planner needs (SM count, max resident warps). */
+int gb_device_info(int device, int *num_sms, int *max_warps_per_sm);
+
+/* ---- L0: counter-based RNG (_rng.py:19-49) -------------------------------
+ * out[i] = draw_below(stream_key(seed, stream, step, vertex0 + i), counter, n)
+ * Used by tests to pin the device RNG against the reference bit-for-bit. */
+int gb_rng_draw_below(uint64_t seed, uint64_t stream, uint64_t step,
+                      uint64_t vertex0, uint64_t counter, int64_t n,
+                      int64_t count, int64_t *out, void *stream_handle);
+
+/* ---- L1: CSR build (graph.py:93-131 _csr_from_arcs / from_edges) ---------
+ * Builds xadj[V+1] (int64) and adj[cap] (int32) from parallel arc arrays.
+ * adj must hold 2*num_arcs entries when GB_CSR_SYMMETRIZE is set, else
+ * num_arcs.  Rows come out strictly ascending and deduplicated.  Synchronizes
+ * and writes the number of stored arcs to *num_edges_out (host pointer). */
+int gb_csr_build_workspace(int64_t num_vertices, int64_t num_arcs,
+                           unsigned flags, size_t *bytes);
+int gb_csr_build(int64_t num_vertices, const int64_t *src, const int64_t *dst,
+                 int64_t num_arcs, unsigned flags, int64_t *xadj, int32_t *adj,
+                 int64_t *num_edges_out, void *workspace, size_t ws_bytes,
+                 void *stream_handle);
+
+/* Drop isolated vertices and re-densify ids in ascending order -- the
+ * load_edge_list convention (graph.py:160-164) applied to a CSR.  new_id
+ * receives the old->new map (-1 for dropped ids); kept receives new->old.
+ * Synchronizes; writes the kept-vertex count to *num_kept_out. */
+int gb_csr_densify_workspace(int64_t num_vertices, size_t *bytes);
+int gb_csr_densify(int64_t num_vertices, int64_t num_edges,
+                   const int64_t *xadj, const int32_t *adj, int64_t *xadj_out,
+                   int32_t *adj_out, int64_t *new_id, int64_t *kept,
+                   int64_t *num_kept_out, void *workspace, size_t ws_bytes,
+                   void *stream_handle);
+
+/* ---- synthetic input: Graph500 R-MAT edge sampler -------
+ * Writes num_samples (src,dst) pairs over 2^scale ids; ids are relabelled by
+ * the seeded permutation perm (perm[i] = i-th id of the stable argsort of
+ * mix-keys, computed by gb_rmat_permutation).  thresholds = {a, a+b, a+b+c}. */
+int gb_rmat_permutation_workspace(int scale, size_t *bytes);
+int gb_rmat_permutation(int scale, uint64_t seed, int64_t *perm,
+                        void *workspace, size_t ws_bytes, void *stream_handle);
+int gb_rmat_edges(int scale, int64_t num_samples, double t_a, double t_ab,
+                  double t_abc, uint64_t seed, const int64_t *perm,
+                  int64_t *src, int64_t *dst, void *stream_handle);
+
+/* ---- L2: coarsening (coarsen.py) ------------------------------------------
+ * degree_order: order[V] by (-deg, +id)   (coarsen.py:69-95 _counting_order) */
+int gb_degree_order_workspace(int64_t num_vertices, size_t *bytes);
+int gb_degree_order(int64_t num_vertices, const int64_t *xadj, int64_t *order,
+                    void *workspace, size_t ws_bytes, void *stream_handle);
+
+/* collapse: cluster map identical to _collapse_seq (coarsen.py:98-114) for
+ * the given order; delta = num_edges/num_vertices as the reference computes
+ * it (coarsen.py:161).  Order-priority rounds, bit-exact by construction
+ * (SURVEY.md Appendix B).  xadj gives the (out-)degrees; in_xadj/in_adj is
+ * the in-arc CSR (the same arrays for an undirected graph, the transpose
+ * for a directed one).  Synchronizes; writes the cluster count. */
+int gb_collapse_workspace(int64_t num_vertices, size_t *bytes);
+int gb_collapse(int64_t num_vertices, const int64_t *xadj, const int64_t *in_xadj,
+                const int32_t *in_adj, const int64_t *order, double delta, int32_t *cmap,
+                int64_t *num_clusters_out, int *rounds_out, void *workspace,
+                size_t ws_bytes, void *stream_handle);
+
+/* coarse CSR: row c = sorted unique {map[u] : u in N(members of c)} \ {c}
+ * (coarsen.py:182-281 build_coarse_graph).  adj_out must hold num_edges
+ * entries.  Synchronizes; writes the coarse arc count. */
+int gb_coarse_csr_workspace(int64_t num_vertices, int64_t num_edges,
+                            int64_t num_clusters, size_t *bytes);
+int gb_coarse_csr(int64_t num_vertices, int64_t num_edges, const int64_t *xadj,
+                  const int32_t *adj, const int32_t *cmap, int64_t num_clusters,
+                  int64_t *xadj_out, int32_t *adj_out, int64_t *num_edges_out,
+                  void *workspace, size_t ws_bytes, void *stream_handle);
+
+/* ---- L3: projection (trainer.py:243-249 expand_embedding) ----------------
+ * out[v, :] = coarse[cmap[v], :] for v < num_rows. */
+int gb_expand(const float *coarse, int64_t num_clusters, int dim,
+              const int32_t *cmap, int64_t num_rows, float *out,
+              void *stream_handle);
+
+/* ---- L3: VERSE/NCE training passes (trainer.py:184-207 _train_pass) ------
+ * Runs passes pass_begin .. pass_begin+n_passes-1 of one level.  Pass p uses
+ * learning rate lr_per_epoch[p / passes_per_epoch] (float32 values, as
+ * train_level computes them, trainer.py:230) and RNG step p.  Sources are
+ * owned by "groups" (G lanes of a warp); max_groups caps how many sources are
+ * in flight at once (0 = fill the GPU).  GB_TRAIN_EXACT runs one group in
+ * the reference's sequential order with the reference's serial fp64 dot and
+ * reproduces _train_pass(num_workers=1) bit-for-bit.  status: see above. */
+int gb_train_passes(int64_t num_vertices, const int64_t *xadj,
+                    const int32_t *adj, float *M, int dim, int n_neg,
+                    uint64_t seed, uint64_t rng_stream, int64_t pass_begin,
+                    int64_t n_passes, int64_t passes_per_epoch,
+                    const float *lr_per_epoch, unsigned flags,
+                    int64_t max_groups, int64_t *status, void *stream_handle);
+
+/* Full-matrix non-finite scan (fallback half of trainer.py:236-237; rows no
+ * update touched).  Sets status[0] and status[1]=epoch when any entry is
+ * NaN/Inf. */
+int gb_nonfinite_scan(const float *M, int64_t count, int64_t epoch,
+                      int64_t *status, void *stream_handle);
+
+/* ---- L3b: partitioned trainer (bigtrain.py) --------------------------------
+ * _fill_pool_side (bigtrain.py:164-196): out[(v-lo_s)*B + t] for v in
+ * [lo_s, hi_s): B uniform draws from N(v) & [lo_t, hi_t), -1 if empty. */
+int gb_fill_pool_side(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
+                      int64_t hi_s, int64_t lo_t, int64_t hi_t, int B,
+                      uint64_t seed, uint64_t side, int32_t *out,
+                      void *stream_handle);
+
+/* _train_pool_side (bigtrain.py:215-238): sources i < n_src of Msrc, B
+ * pooled targets each (global ids, minus lo_t), n_neg negatives drawn from
+ * [0, n_t) with key(seed, side, 1, i).  lr is float64 as in train_large
+ * (bigtrain.py:432).  When Msrc == Mtgt (diagonal pair) a self-sample uses
+ * the load-once rule of the reference's noalias kernel.
+ * If targets == NULL the pool is drawn on the fly from the device CSR
+ * (xadj/adj, source ids lo_s + i, pool side pool_side, pool key
+ * key(seed, pool_side, 0, v)) -- bit-identical to a materialized pool.
+ * status[2] += positive updates applied. */
+int gb_train_pool_side(float *Msrc, float *Mtgt, int dim,
+                       const int32_t *targets, int64_t n_src, int B,
+                       int64_t lo_t, int64_t n_t, int n_neg, double lr,
+                       uint64_t seed, uint64_t side, const int64_t *xadj,
+                       const int32_t *adj, int64_t lo_s, uint64_t pool_side,
+                       unsigned flags, int64_t max_groups, int64_t *status,
+                       void *stream_handle);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GOSH_B200_H */

@@ -1,0 +1,745 @@
+// Graph-side kernels: CSR construction (graph.py:93-131), id densification
+// (graph.py:160-164), the R-MAT input generator, degree order
+// (coarsen.py:69-95), the order-priority MultiEdgeCollapse (coarsen.py:98-114,
+// restated in SURVEY.md Appendix B), coarse CSR (coarsen.py:182-281) and the
+// coarse-to-fine projection (trainer.py:243-249).
+//
+// All of it is integer/byte work bounded by HBM: arcs are mapped to 64-bit
+// (row, col) keys, radix-sorted, run-length deduplicated and turned into
+// row offsets by a per-row binary search -- the sorted unique key sequence IS
+// the CSR, so the result is bit-identical to the reference's numpy/numba
+// construction by definition.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace gb {
+namespace {
+
+constexpr uint64_t kRmatStream = 0x524D4154ull;  // "RMAT"
+constexpr uint64_t kPermStream = 0x5045524Dull;  // "PERM"
+constexpr int8_t kUndecided = 0, kHub = 1, kMember = 2;
+
+// Carves 256-byte aligned sub-buffers out of a caller workspace.  With a
+// null base it only accumulates the size (workspace queries).
+struct Carver {
+  char *base;
+  size_t off = 0;
+  explicit Carver(void *b) : base(static_cast<char *>(b)) {}
+  template <class T>
+  T *take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+    off += n * sizeof(T);
+    return p;
+  }
+  void *take_bytes(size_t n) { return take<char>(n); }
+};
+
+inline int bits_for(uint64_t x) {  // number of bits to represent values <= x
+  int b = 0;
+  while (b < 64 && (x >> b) != 0) ++b;
+  return std::max(b, 1);
+}
+
+inline int blocks_for(int64_t n, int threads = 256) {
+  int64_t b = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms() * 32;
+  return (int)std::max<int64_t>(1, std::min(b, cap));
+}
+
+#define GRID_STRIDE(i, n)                                                   \
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); \
+       i += (int64_t)gridDim.x * blockDim.x)
+
+// ---------------------------------------------------------------------------
+// sorted-key -> CSR helpers
+// ---------------------------------------------------------------------------
+__global__ void keys_from_arcs(const int64_t *__restrict__ src, const int64_t *__restrict__ dst,
+                               int64_t n, int64_t V, bool drop_self, bool sym, uint64_t sentinel,
+                               uint64_t *__restrict__ keys) {
+  GRID_STRIDE(i, n) {
+    const int64_t s = src[i], d = dst[i];
+    const bool self = drop_self && s == d;
+    keys[i] = self ? sentinel : (uint64_t)s * (uint64_t)V + (uint64_t)d;
+    if (sym) keys[n + i] = self ? sentinel : (uint64_t)d * (uint64_t)V + (uint64_t)s;
+  }
+}
+
+// xadj[r] = lower_bound(keys, r*V) over the sorted unique keys.
+__global__ void xadj_from_keys(const uint64_t *__restrict__ keys, int64_t nkeys, int64_t V,
+                               int64_t *__restrict__ xadj) {
+  GRID_STRIDE(r, V + 1) {
+    const uint64_t target = (uint64_t)r * (uint64_t)V;
+    int64_t lo = 0, hi = nkeys;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < target)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    xadj[r] = lo;
+  }
+}
+
+__global__ void adj_from_keys(const uint64_t *__restrict__ keys, int64_t nkeys, int64_t V,
+                              int32_t *__restrict__ adj) {
+  GRID_STRIDE(i, nkeys) adj[i] = (int32_t)(keys[i] % (uint64_t)V);
+}
+
+// Sort keys, deduplicate, strip the sentinel tail, emit xadj/adj.  Shared by
+// the CSR build and the coarse-graph build.
+struct KeyCsrBuffers {
+  uint64_t *keys_alt;
+  uint64_t *uniq;
+  int64_t *num_sel;
+  void *cub_tmp;
+  size_t cub_bytes;
+};
+
+int key_csr_carve(Carver &c, int64_t n, int end_bit, KeyCsrBuffers &b) {
+  b.keys_alt = c.take<uint64_t>(n);
+  b.uniq = c.take<uint64_t>(n);
+  b.num_sel = c.take<int64_t>(1);
+  size_t sort_bytes = 0, uniq_bytes = 0;
+  GB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, sort_bytes, (uint64_t *)nullptr,
+                                             (uint64_t *)nullptr, n, 0, end_bit));
+  GB_CUDA_TRY(cub::DeviceSelect::Unique(nullptr, uniq_bytes, (uint64_t *)nullptr,
+                                        (uint64_t *)nullptr, (int64_t *)nullptr, n));
+  b.cub_bytes = std::max(sort_bytes, uniq_bytes);
+  b.cub_tmp = c.take_bytes(b.cub_bytes);
+  return GB_OK;
+}
+
+int keys_to_csr(uint64_t *keys, int64_t n, int end_bit, int64_t V, uint64_t sentinel,
+                KeyCsrBuffers &b, int64_t *xadj, int32_t *adj, int64_t *num_edges_out,
+                cudaStream_t st) {
+  int64_t nuniq = 0;
+  if (n > 0) {
+    size_t tb = b.cub_bytes;
+    GB_CUDA_TRY(
+        cub::DeviceRadixSort::SortKeys(b.cub_tmp, tb, keys, b.keys_alt, n, 0, end_bit, st));
+    tb = b.cub_bytes;
+    GB_CUDA_TRY(cub::DeviceSelect::Unique(b.cub_tmp, tb, b.keys_alt, b.uniq, b.num_sel, n, st));
+    GB_CUDA_TRY(cudaMemcpyAsync(&nuniq, b.num_sel, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GB_CUDA_TRY(cudaStreamSynchronize(st));
+    if (nuniq > 0) {
+      uint64_t last = 0;
+      GB_CUDA_TRY(cudaMemcpyAsync(&last, b.uniq + nuniq - 1, sizeof(uint64_t),
+                                  cudaMemcpyDeviceToHost, st));
+      GB_CUDA_TRY(cudaStreamSynchronize(st));
+      if (last == sentinel) --nuniq;
+    }
+  }
+  xadj_from_keys<<<blocks_for(V + 1), 256, 0, st>>>(b.uniq, nuniq, V, xadj);
+  GB_CHECK_LAUNCH();
+  if (nuniq > 0) {
+    adj_from_keys<<<blocks_for(nuniq), 256, 0, st>>>(b.uniq, nuniq, V, adj);
+    GB_CHECK_LAUNCH();
+  }
+  GB_CUDA_TRY(cudaStreamSynchronize(st));
+  *num_edges_out = nuniq;
+  return GB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// densify
+// ---------------------------------------------------------------------------
+__global__ void nonisolated_flags(const int64_t *__restrict__ xadj, int64_t V,
+                                  int64_t *__restrict__ flag) {
+  GRID_STRIDE(v, V) flag[v] = xadj[v + 1] > xadj[v] ? 1 : 0;
+}
+
+__global__ void densify_vertices(const int64_t *__restrict__ xadj, const int64_t *__restrict__ pos,
+                                 int64_t V, int64_t *__restrict__ new_id,
+                                 int64_t *__restrict__ kept, int64_t *__restrict__ xadj_out) {
+  GRID_STRIDE(v, V) {
+    if (xadj[v + 1] > xadj[v]) {
+      const int64_t k = pos[v];
+      new_id[v] = k;
+      kept[k] = v;
+      xadj_out[k] = xadj[v];  // removing empty rows does not move arcs
+    } else {
+      new_id[v] = -1;
+    }
+  }
+}
+
+__global__ void remap_adj(const int32_t *__restrict__ adj, int64_t E,
+                          const int64_t *__restrict__ new_id, int32_t *__restrict__ adj_out) {
+  GRID_STRIDE(e, E) adj_out[e] = (int32_t)new_id[adj[e]];
+}
+
+__global__ void set_tail(int64_t *__restrict__ xadj_out, const int64_t *__restrict__ count,
+                         int64_t E) {
+  xadj_out[*count] = E;
+}
+
+// ---------------------------------------------------------------------------
+// R-MAT
+// ---------------------------------------------------------------------------
+__global__ void perm_keys(int64_t n, uint64_t pkey, uint64_t *__restrict__ keys,
+                          int64_t *__restrict__ ids) {
+  GRID_STRIDE(i, n) {
+    keys[i] = draw_u64(pkey, (uint64_t)i);
+    ids[i] = i;
+  }
+}
+
+__global__ void rmat_kernel(int scale, int64_t n, double ta, double tab, double tabc,
+                            uint64_t seed, const int64_t *__restrict__ perm,
+                            int64_t *__restrict__ src, int64_t *__restrict__ dst) {
+  GRID_STRIDE(e, n) {
+    const uint64_t key = stream_key(seed, kRmatStream, (uint64_t)e, 0);
+    int64_t u = 0, v = 0;
+    for (int l = 0; l < scale; ++l) {
+      const double r = draw_unit(key, (uint64_t)l);
+      const int64_t bit = int64_t(1) << (scale - 1 - l);
+      if (r < ta) {
+      } else if (r < tab) {
+        v |= bit;
+      } else if (r < tabc) {
+        u |= bit;
+      } else {
+        u |= bit;
+        v |= bit;
+      }
+    }
+    src[e] = perm ? perm[u] : u;
+    dst[e] = perm ? perm[v] : v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// degree order
+// ---------------------------------------------------------------------------
+__global__ void degrees_kernel(const int64_t *__restrict__ xadj, int64_t V,
+                               uint64_t *__restrict__ deg, int64_t *__restrict__ ids) {
+  GRID_STRIDE(v, V) {
+    deg[v] = (uint64_t)(xadj[v + 1] - xadj[v]);
+    ids[v] = v;
+  }
+}
+
+__global__ void invert_degree_keys(uint64_t *__restrict__ deg, int64_t V,
+                                   const uint64_t *__restrict__ maxdeg) {
+  const uint64_t m = *maxdeg;
+  GRID_STRIDE(v, V) deg[v] = m - deg[v];
+}
+
+// ---------------------------------------------------------------------------
+// collapse: u is a HUB iff no H-in-neighbour is a hub;
+// a member joins its minimum-rank hub H-in-neighbour.  H-in-neighbours of u:
+// w adjacent to u with rank(w) < rank(u) and (small(w) or small(u)).  A vertex
+// that is not small has none (a small w has lower degree, hence higher rank),
+// so it is a hub outright.
+// ---------------------------------------------------------------------------
+__global__ void collapse_init(const int64_t *__restrict__ xadj, const int64_t *__restrict__ order,
+                              int64_t V, double delta, int64_t *__restrict__ rank,
+                              int8_t *__restrict__ status) {
+  GRID_STRIDE(i, V) {
+    const int64_t v = order[i];
+    rank[v] = i;
+    const double deg = (double)(xadj[v + 1] - xadj[v]);
+    status[v] = deg <= delta ? kUndecided : kHub;  // coarsen.py:108,111
+  }
+}
+
+// One Gauss-Seidel round over the undecided vertices.  Reading a neighbour's
+// status written in this same round is safe: decisions are monotone.
+__global__ void collapse_round(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
+                               const int64_t *__restrict__ rank, int64_t V,
+                               volatile int8_t *status, unsigned long long *undecided) {
+  unsigned long long left = 0;
+  GRID_STRIDE(u, V) {
+    if (status[u] != kUndecided) continue;
+    const int64_t ru = rank[u];
+    bool any_hub = false, all_member = true;
+    for (int64_t e = xadj[u]; e < xadj[u + 1]; ++e) {
+      const int64_t w = adj[e];
+      if (rank[w] >= ru) continue;
+      const int8_t sw = status[w];
+      if (sw == kHub) {
+        any_hub = true;
+        break;
+      }
+      if (sw != kMember) all_member = false;
+    }
+    if (any_hub)
+      status[u] = kMember;
+    else if (all_member)
+      status[u] = kHub;
+    else
+      ++left;
+  }
+  if (left) atomicAdd(undecided, left);
+}
+
+// Exact sequential finish for pathological chains: walk the order once; every
+// lower-rank vertex is decided by the time u is reached.  One warp.
+__global__ void collapse_tail(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
+                              const int64_t *__restrict__ rank, const int64_t *__restrict__ order,
+                              int64_t V, volatile int8_t *status) {
+  const int lane = threadIdx.x;
+  for (int64_t i = 0; i < V; ++i) {
+    const int64_t u = order[i];
+    if (status[u] != kUndecided) continue;
+    bool hub_nbr = false;
+    for (int64_t e = xadj[u] + lane; e < xadj[u + 1]; e += 32) {
+      const int64_t w = adj[e];
+      if (rank[w] < i && status[w] == kHub) hub_nbr = true;
+    }
+    hub_nbr = __any_sync(0xffffffffu, hub_nbr);
+    if (lane == 0) status[u] = hub_nbr ? kMember : kHub;
+    __syncwarp();
+    __threadfence_block();
+  }
+}
+
+__global__ void hub_flags_by_rank(const int64_t *__restrict__ order,
+                                  const int8_t *__restrict__ status, int64_t V,
+                                  int64_t *__restrict__ flag) {
+  GRID_STRIDE(i, V) flag[i] = status[order[i]] == kHub ? 1 : 0;
+}
+
+__global__ void assign_clusters(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
+                                const int64_t *__restrict__ rank,
+                                const int8_t *__restrict__ status,
+                                const int64_t *__restrict__ cid_by_rank, int64_t V,
+                                int32_t *__restrict__ cmap) {
+  GRID_STRIDE(u, V) {
+    const int64_t ru = rank[u];
+    if (status[u] == kHub) {
+      cmap[u] = (int32_t)cid_by_rank[ru];
+      continue;
+    }
+    int64_t best = INT64_MAX;
+    for (int64_t e = xadj[u]; e < xadj[u + 1]; ++e) {
+      const int64_t w = adj[e];
+      const int64_t rw = rank[w];
+      if (rw < ru && rw < best && status[w] == kHub) best = rw;
+    }
+    cmap[u] = (int32_t)cid_by_rank[best];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// coarse CSR keys: warp per vertex, lanes over its arcs (coalesced).
+// ---------------------------------------------------------------------------
+__global__ void coarse_keys(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
+                            const int32_t *__restrict__ cmap, int64_t V, uint64_t nc,
+                            uint64_t sentinel, uint64_t *__restrict__ keys) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < V; v += nwarps) {
+    const uint64_t cv = (uint64_t)cmap[v];
+    const int64_t e1 = xadj[v + 1];
+    for (int64_t e = xadj[v] + lane; e < e1; e += 32) {
+      const uint64_t cu = (uint64_t)cmap[adj[e]];
+      keys[e] = cu == cv ? sentinel : cv * nc + cu;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// expand
+// ---------------------------------------------------------------------------
+__global__ void expand_vec4(const float4 *__restrict__ coarse, const int32_t *__restrict__ cmap,
+                            int64_t rows, int q, float4 *__restrict__ out) {
+  GRID_STRIDE(i, rows * q) {
+    const int64_t v = i / q;
+    const int64_t c = i - v * q;
+    out[i] = __ldg(coarse + (int64_t)cmap[v] * q + c);
+  }
+}
+
+__global__ void expand_scalar(const float *__restrict__ coarse, const int32_t *__restrict__ cmap,
+                              int64_t rows, int dim, float *__restrict__ out) {
+  GRID_STRIDE(i, rows * dim) {
+    const int64_t v = i / dim;
+    const int64_t c = i - v * dim;
+    out[i] = __ldg(coarse + (int64_t)cmap[v] * dim + c);
+  }
+}
+
+__global__ void rng_draw_kernel(uint64_t seed, uint64_t stream, uint64_t step, uint64_t v0,
+                                uint64_t ctr, int64_t n, int64_t count, int64_t *out) {
+  GRID_STRIDE(i, count) out[i] = draw_below(stream_key(seed, stream, step, v0 + i), ctr, n);
+}
+
+}  // namespace
+}  // namespace gb
+
+using namespace gb;
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+GB_API int gb_rng_draw_below(uint64_t seed, uint64_t stream, uint64_t step, uint64_t vertex0,
+                                 uint64_t counter, int64_t n, int64_t count, int64_t *out,
+                                 void *stream_handle) {
+  GB_REQUIRE(n > 0 && count >= 0 && out, "gb_rng_draw_below: bad args");
+  if (count == 0) return GB_OK;
+  rng_draw_kernel<<<blocks_for(count), 256, 0, as_stream(stream_handle)>>>(
+      seed, stream, step, vertex0, counter, n, count, out);
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
+static int csr_build_layout(Carver &c, int64_t V, int64_t num_arcs, unsigned flags,
+                            uint64_t **keys, KeyCsrBuffers &b, int *end_bit, uint64_t *sentinel) {
+  const int64_t n = num_arcs * ((flags & GB_CSR_SYMMETRIZE) ? 2 : 1);
+  *sentinel = (uint64_t)V * (uint64_t)V;
+  *end_bit = bits_for(*sentinel);
+  *keys = c.take<uint64_t>(n);
+  return key_csr_carve(c, n, *end_bit, b);
+}
+
+GB_API int gb_csr_build_workspace(int64_t num_vertices, int64_t num_arcs, unsigned flags,
+                                      size_t *bytes) {
+  GB_REQUIRE(num_vertices >= 1 && num_vertices < (int64_t(1) << 31) && num_arcs >= 0 && bytes,
+             "gb_csr_build_workspace: bad args");
+  Carver c(nullptr);
+  uint64_t *keys;
+  KeyCsrBuffers b;
+  int end_bit;
+  uint64_t sentinel;
+  int rc = csr_build_layout(c, num_vertices, num_arcs, flags, &keys, b, &end_bit, &sentinel);
+  if (rc) return rc;
+  *bytes = c.off + 256;
+  return GB_OK;
+}
+
+GB_API int gb_csr_build(int64_t num_vertices, const int64_t *src, const int64_t *dst,
+                            int64_t num_arcs, unsigned flags, int64_t *xadj, int32_t *adj,
+                            int64_t *num_edges_out, void *workspace, size_t ws_bytes,
+                            void *stream_handle) {
+  GB_REQUIRE(num_vertices >= 1 && num_vertices < (int64_t(1) << 31) && num_arcs >= 0,
+             "gb_csr_build: bad sizes");
+  GB_REQUIRE(xadj && num_edges_out && (num_arcs == 0 || (src && dst && adj)),
+             "gb_csr_build: null pointer");
+  Carver c(workspace);
+  uint64_t *keys;
+  KeyCsrBuffers b;
+  int end_bit;
+  uint64_t sentinel;
+  int rc = csr_build_layout(c, num_vertices, num_arcs, flags, &keys, b, &end_bit, &sentinel);
+  if (rc) return rc;
+  GB_REQUIRE(c.off <= ws_bytes, "gb_csr_build: workspace %zu < %zu", ws_bytes, c.off);
+  cudaStream_t st = as_stream(stream_handle);
+  const int64_t n = num_arcs * ((flags & GB_CSR_SYMMETRIZE) ? 2 : 1);
+  if (num_arcs > 0) {
+    keys_from_arcs<<<blocks_for(num_arcs), 256, 0, st>>>(
+        src, dst, num_arcs, num_vertices, (flags & GB_CSR_DROP_SELF) != 0,
+        (flags & GB_CSR_SYMMETRIZE) != 0, sentinel, keys);
+    GB_CHECK_LAUNCH();
+  }
+  return keys_to_csr(keys, n, end_bit, num_vertices, sentinel, b, xadj, adj, num_edges_out, st);
+}
+
+GB_API int gb_csr_densify_workspace(int64_t num_vertices, size_t *bytes) {
+  GB_REQUIRE(num_vertices >= 1 && bytes, "gb_csr_densify_workspace: bad args");
+  Carver c(nullptr);
+  c.take<int64_t>(num_vertices);
+  c.take<int64_t>(num_vertices);
+  c.take<int64_t>(1);
+  size_t scan_bytes = 0;
+  GB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int64_t *)nullptr,
+                                            (int64_t *)nullptr, num_vertices + 1));
+  c.take_bytes(scan_bytes);
+  *bytes = c.off + 256;
+  return GB_OK;
+}
+
+GB_API int gb_csr_densify(int64_t num_vertices, int64_t num_edges, const int64_t *xadj,
+                              const int32_t *adj, int64_t *xadj_out, int32_t *adj_out,
+                              int64_t *new_id, int64_t *kept, int64_t *num_kept_out,
+                              void *workspace, size_t ws_bytes, void *stream_handle) {
+  GB_REQUIRE(num_vertices >= 1 && num_edges >= 0 && xadj && xadj_out && new_id && kept &&
+                 num_kept_out,
+             "gb_csr_densify: bad args");
+  cudaStream_t st = as_stream(stream_handle);
+  Carver c(workspace);
+  int64_t *flag = c.take<int64_t>(num_vertices + 1);
+  int64_t *pos = c.take<int64_t>(num_vertices + 1);
+  int64_t *cnt = c.take<int64_t>(1);
+  size_t scan_bytes = 0;
+  GB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, flag, pos, num_vertices + 1));
+  void *tmp = c.take_bytes(scan_bytes);
+  GB_REQUIRE(c.off <= ws_bytes, "gb_csr_densify: workspace too small");
+  GB_CUDA_TRY(cudaMemsetAsync(flag + num_vertices, 0, sizeof(int64_t), st));
+  nonisolated_flags<<<blocks_for(num_vertices), 256, 0, st>>>(xadj, num_vertices, flag);
+  GB_CHECK_LAUNCH();
+  GB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, flag, pos, num_vertices + 1, st));
+  densify_vertices<<<blocks_for(num_vertices), 256, 0, st>>>(xadj, pos, num_vertices, new_id,
+                                                              kept, xadj_out);
+  GB_CHECK_LAUNCH();
+  GB_CUDA_TRY(cudaMemcpyAsync(cnt, pos + num_vertices, sizeof(int64_t), cudaMemcpyDeviceToDevice,
+                              st));
+  set_tail<<<1, 1, 0, st>>>(xadj_out, cnt, num_edges);
+  GB_CHECK_LAUNCH();
+  if (num_edges > 0) {
+    remap_adj<<<blocks_for(num_edges), 256, 0, st>>>(adj, num_edges, new_id, adj_out);
+    GB_CHECK_LAUNCH();
+  }
+  int64_t nk = 0;
+  GB_CUDA_TRY(cudaMemcpyAsync(&nk, cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GB_CUDA_TRY(cudaStreamSynchronize(st));
+  *num_kept_out = nk;
+  return GB_OK;
+}
+
+GB_API int gb_rmat_permutation_workspace(int scale, size_t *bytes) {
+  GB_REQUIRE(scale >= 1 && scale <= 34 && bytes, "gb_rmat_permutation_workspace: bad args");
+  const int64_t n = int64_t(1) << scale;
+  Carver c(nullptr);
+  c.take<uint64_t>(n);
+  c.take<uint64_t>(n);
+  c.take<int64_t>(n);
+  size_t sb = 0;
+  GB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, sb, (uint64_t *)nullptr,
+                                              (uint64_t *)nullptr, (int64_t *)nullptr,
+                                              (int64_t *)nullptr, n));
+  c.take_bytes(sb);
+  *bytes = c.off + 256;
+  return GB_OK;
+}
+
+GB_API int gb_rmat_permutation(int scale, uint64_t seed, int64_t *perm, void *workspace,
+                                   size_t ws_bytes, void *stream_handle) {
+  GB_REQUIRE(scale >= 1 && scale <= 34 && perm, "gb_rmat_permutation: bad args");
+  const int64_t n = int64_t(1) << scale;
+  cudaStream_t st = as_stream(stream_handle);
+  Carver c(workspace);
+  uint64_t *k0 = c.take<uint64_t>(n);
+  uint64_t *k1 = c.take<uint64_t>(n);
+  int64_t *ids = c.take<int64_t>(n);
+  size_t sb = 0;
+  GB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, sb, k0, k1, ids, perm, n));
+  void *tmp = c.take_bytes(sb);
+  GB_REQUIRE(c.off <= ws_bytes, "gb_rmat_permutation: workspace too small");
+  perm_keys<<<blocks_for(n), 256, 0, st>>>(n, stream_key(seed, kPermStream, 0, 0), k0, ids);
+  GB_CHECK_LAUNCH();
+  GB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, sb, k0, k1, ids, perm, n, 0, 64, st));
+  return GB_OK;
+}
+
+GB_API int gb_rmat_edges(int scale, int64_t num_samples, double t_a, double t_ab,
+                             double t_abc, uint64_t seed, const int64_t *perm, int64_t *src,
+                             int64_t *dst, void *stream_handle) {
+  GB_REQUIRE(scale >= 1 && scale <= 34 && num_samples >= 0 && src && dst,
+             "gb_rmat_edges: bad args");
+  if (num_samples == 0) return GB_OK;
+  rmat_kernel<<<blocks_for(num_samples), 256, 0, as_stream(stream_handle)>>>(
+      scale, num_samples, t_a, t_ab, t_abc, seed, perm, src, dst);
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
+static int degree_order_layout(Carver &c, int64_t V, uint64_t **deg, uint64_t **deg_alt,
+                               int64_t **ids, uint64_t **maxdeg, void **tmp, size_t *tb) {
+  *deg = c.take<uint64_t>(V);
+  *deg_alt = c.take<uint64_t>(V);
+  *ids = c.take<int64_t>(V);
+  *maxdeg = c.take<uint64_t>(1);
+  size_t s1 = 0, s2 = 0;
+  GB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, s1, (uint64_t *)nullptr,
+                                              (uint64_t *)nullptr, (int64_t *)nullptr,
+                                              (int64_t *)nullptr, V));
+  GB_CUDA_TRY(cub::DeviceReduce::Max(nullptr, s2, (uint64_t *)nullptr, (uint64_t *)nullptr, V));
+  *tb = std::max(s1, s2);
+  *tmp = c.take_bytes(*tb);
+  return GB_OK;
+}
+
+GB_API int gb_degree_order_workspace(int64_t num_vertices, size_t *bytes) {
+  GB_REQUIRE(num_vertices >= 1 && bytes, "gb_degree_order_workspace: bad args");
+  Carver c(nullptr);
+  uint64_t *a, *b, *m;
+  int64_t *ids;
+  void *tmp;
+  size_t tb;
+  int rc = degree_order_layout(c, num_vertices, &a, &b, &ids, &m, &tmp, &tb);
+  if (rc) return rc;
+  *bytes = c.off + 256;
+  return GB_OK;
+}
+
+GB_API int gb_degree_order(int64_t num_vertices, const int64_t *xadj, int64_t *order,
+                               void *workspace, size_t ws_bytes, void *stream_handle) {
+  GB_REQUIRE(num_vertices >= 1 && xadj && order, "gb_degree_order: bad args");
+  cudaStream_t st = as_stream(stream_handle);
+  Carver c(workspace);
+  uint64_t *deg, *deg_alt, *maxdeg;
+  int64_t *ids;
+  void *tmp;
+  size_t tb;
+  int rc = degree_order_layout(c, num_vertices, &deg, &deg_alt, &ids, &maxdeg, &tmp, &tb);
+  if (rc) return rc;
+  GB_REQUIRE(c.off <= ws_bytes, "gb_degree_order: workspace too small");
+  degrees_kernel<<<blocks_for(num_vertices), 256, 0, st>>>(xadj, num_vertices, deg, ids);
+  GB_CHECK_LAUNCH();
+  size_t t1 = tb;
+  GB_CUDA_TRY(cub::DeviceReduce::Max(tmp, t1, deg, maxdeg, num_vertices, st));
+  invert_degree_keys<<<blocks_for(num_vertices), 256, 0, st>>>(deg, num_vertices, maxdeg);
+  GB_CHECK_LAUNCH();
+  // stable LSD radix sort: ties (equal degree) keep ascending id order
+  t1 = tb;
+  GB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, t1, deg, deg_alt, ids, order, num_vertices, 0,
+                                              64, st));
+  return GB_OK;
+}
+
+static int collapse_layout(Carver &c, int64_t V, int64_t **rank, int8_t **status,
+                           int64_t **flag, int64_t **cid, unsigned long long **undecided,
+                           void **tmp, size_t *tb) {
+  *rank = c.take<int64_t>(V);
+  *status = c.take<int8_t>(V);
+  *flag = c.take<int64_t>(V + 1);
+  *cid = c.take<int64_t>(V + 1);
+  *undecided = c.take<unsigned long long>(1);
+  *tb = 0;
+  GB_CUDA_TRY(
+      cub::DeviceScan::ExclusiveSum(nullptr, *tb, (int64_t *)nullptr, (int64_t *)nullptr, V + 1));
+  *tmp = c.take_bytes(*tb);
+  return GB_OK;
+}
+
+GB_API int gb_collapse_workspace(int64_t num_vertices, size_t *bytes) {
+  GB_REQUIRE(num_vertices >= 1 && bytes, "gb_collapse_workspace: bad args");
+  Carver c(nullptr);
+  int64_t *r, *f, *cid;
+  int8_t *s;
+  unsigned long long *u;
+  void *tmp;
+  size_t tb;
+  int rc = collapse_layout(c, num_vertices, &r, &s, &f, &cid, &u, &tmp, &tb);
+  if (rc) return rc;
+  *bytes = c.off + 256;
+  return GB_OK;
+}
+
+GB_API int gb_collapse(int64_t num_vertices, const int64_t *xadj, const int64_t *in_xadj,
+                           const int32_t *in_adj, const int64_t *order, double delta, int32_t *cmap,
+                           int64_t *num_clusters_out, int *rounds_out, void *workspace,
+                           size_t ws_bytes, void *stream_handle) {
+  GB_REQUIRE(num_vertices >= 1 && xadj && in_xadj && order && cmap && num_clusters_out,
+             "gb_collapse: bad args");
+  const int64_t V = num_vertices;
+  cudaStream_t st = as_stream(stream_handle);
+  Carver c(workspace);
+  int64_t *rank, *flag, *cid;
+  int8_t *status;
+  unsigned long long *undecided;
+  void *tmp;
+  size_t tb;
+  int rc = collapse_layout(c, V, &rank, &status, &flag, &cid, &undecided, &tmp, &tb);
+  if (rc) return rc;
+  GB_REQUIRE(c.off <= ws_bytes, "gb_collapse: workspace too small");
+  collapse_init<<<blocks_for(V), 256, 0, st>>>(xadj, order, V, delta, rank, status);
+  GB_CHECK_LAUNCH();
+  const int kMaxRounds = 24;
+  int rounds = 0;
+  unsigned long long left = 1;
+  while (left > 0 && rounds < kMaxRounds) {
+    GB_CUDA_TRY(cudaMemsetAsync(undecided, 0, sizeof(unsigned long long), st));
+    collapse_round<<<blocks_for(V), 256, 0, st>>>(in_xadj, in_adj, rank, V, status, undecided);
+    GB_CHECK_LAUNCH();
+    GB_CUDA_TRY(
+        cudaMemcpyAsync(&left, undecided, sizeof(left), cudaMemcpyDeviceToHost, st));
+    GB_CUDA_TRY(cudaStreamSynchronize(st));
+    ++rounds;
+  }
+  if (left > 0) {
+    collapse_tail<<<1, 32, 0, st>>>(in_xadj, in_adj, rank, order, V, status);
+    GB_CHECK_LAUNCH();
+    ++rounds;
+  }
+  GB_CUDA_TRY(cudaMemsetAsync(flag + V, 0, sizeof(int64_t), st));
+  hub_flags_by_rank<<<blocks_for(V), 256, 0, st>>>(order, status, V, flag);
+  GB_CHECK_LAUNCH();
+  GB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flag, cid, V + 1, st));
+  assign_clusters<<<blocks_for(V), 256, 0, st>>>(in_xadj, in_adj, rank, status, cid, V, cmap);
+  GB_CHECK_LAUNCH();
+  int64_t nc = 0;
+  GB_CUDA_TRY(cudaMemcpyAsync(&nc, cid + V, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GB_CUDA_TRY(cudaStreamSynchronize(st));
+  *num_clusters_out = nc;
+  if (rounds_out) *rounds_out = rounds;
+  return GB_OK;
+}
+
+static int coarse_layout(Carver &c, int64_t E, int64_t nc, uint64_t **keys, KeyCsrBuffers &b,
+                         int *end_bit, uint64_t *sentinel) {
+  *sentinel = (uint64_t)nc * (uint64_t)nc;
+  *end_bit = bits_for(*sentinel);
+  *keys = c.take<uint64_t>(E);
+  return key_csr_carve(c, E, *end_bit, b);
+}
+
+GB_API int gb_coarse_csr_workspace(int64_t num_vertices, int64_t num_edges,
+                                       int64_t num_clusters, size_t *bytes) {
+  GB_REQUIRE(num_vertices >= 1 && num_edges >= 0 && num_clusters >= 1 && bytes,
+             "gb_coarse_csr_workspace: bad args");
+  Carver c(nullptr);
+  uint64_t *keys;
+  KeyCsrBuffers b;
+  int eb;
+  uint64_t sent;
+  int rc = coarse_layout(c, num_edges, num_clusters, &keys, b, &eb, &sent);
+  if (rc) return rc;
+  *bytes = c.off + 256;
+  return GB_OK;
+}
+
+GB_API int gb_coarse_csr(int64_t num_vertices, int64_t num_edges, const int64_t *xadj,
+                             const int32_t *adj, const int32_t *cmap, int64_t num_clusters,
+                             int64_t *xadj_out, int32_t *adj_out, int64_t *num_edges_out,
+                             void *workspace, size_t ws_bytes, void *stream_handle) {
+  GB_REQUIRE(num_vertices >= 1 && num_edges >= 0 && num_clusters >= 1 && xadj && cmap &&
+                 xadj_out && num_edges_out,
+             "gb_coarse_csr: bad args");
+  cudaStream_t st = as_stream(stream_handle);
+  Carver c(workspace);
+  uint64_t *keys;
+  KeyCsrBuffers b;
+  int end_bit;
+  uint64_t sentinel;
+  int rc = coarse_layout(c, num_edges, num_clusters, &keys, b, &end_bit, &sentinel);
+  if (rc) return rc;
+  GB_REQUIRE(c.off <= ws_bytes, "gb_coarse_csr: workspace too small");
+  if (num_edges > 0) {
+    int blocks = (int)std::min<int64_t>((num_vertices + 7) / 8, (int64_t)num_sms() * 16);
+    coarse_keys<<<std::max(blocks, 1), 256, 0, st>>>(xadj, adj, cmap, num_vertices,
+                                                     (uint64_t)num_clusters, sentinel, keys);
+    GB_CHECK_LAUNCH();
+  }
+  return keys_to_csr(keys, num_edges, end_bit, num_clusters, sentinel, b, xadj_out, adj_out,
+                     num_edges_out, st);
+}
+
+GB_API int gb_expand(const float *coarse, int64_t num_clusters, int dim, const int32_t *cmap,
+                         int64_t num_rows, float *out, void *stream_handle) {
+  GB_REQUIRE(coarse && cmap && out && dim >= 1 && num_rows >= 0 && num_clusters >= 1,
+             "gb_expand: bad args");
+  if (num_rows == 0) return GB_OK;
+  cudaStream_t st = as_stream(stream_handle);
+  const bool vec = dim % 4 == 0 && (reinterpret_cast<uintptr_t>(coarse) & 15u) == 0 &&
+                   (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+  if (vec) {
+    const int q = dim / 4;
+    expand_vec4<<<blocks_for(num_rows * q), 256, 0, st>>>(
+        reinterpret_cast<const float4 *>(coarse), cmap, num_rows, q,
+        reinterpret_cast<float4 *>(out));
+  } else {
+    expand_scalar<<<blocks_for(num_rows * dim), 256, 0, st>>>(coarse, cmap, num_rows, dim, out);
+  }
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}

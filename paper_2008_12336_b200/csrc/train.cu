@@ -1,0 +1,165 @@
+// C ABI of the training kernels: layout dispatch, grid sizing, launch.
+// Kernels live in train_kernels.cuh; instantiations in train_{vec_*,scalar}.cu.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+
+#include "train_kernels.cuh"
+
+namespace gb {
+namespace tk {
+
+Variant vec_variant_a(int G, int NV);
+Variant vec_variant_b(int G, int NV);
+Variant vec_variant_c(int G, int NV);
+
+Variant vec_variant(int G, int NV) {
+  Variant v = vec_variant_a(G, NV);
+  if (!v.G) v = vec_variant_b(G, NV);
+  if (!v.G) v = vec_variant_c(G, NV);
+  return v;
+}
+
+namespace {
+
+__global__ void nonfinite_scan_kernel(const float *__restrict__ M, int64_t n, int64_t epoch,
+                                      int64_t *status) {
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(M[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) {
+    atomicOr(reinterpret_cast<unsigned long long *>(status), 1ull);
+    atomicMin(reinterpret_cast<long long *>(status + 1), (long long)epoch);
+  }
+}
+
+// Default lanes per source for a vector layout; GB_GROUP_LANES overrides it
+// (tuning knob; the layout only changes the tree-dot summation order).
+int preferred_lanes(int dim) {
+  const char *env = std::getenv("GB_GROUP_LANES");
+  if (env) {
+    int g = std::atoi(env);
+    if (g == 2 || g == 4 || g == 8 || g == 16 || g == 32) return g;
+  }
+  if (dim <= 16) return std::max(dim / 4, 2);
+  if (dim <= 128) return 8;
+  return 16;
+}
+
+bool pick_vector(int dim, int G, Variant &out) {
+  if (dim % 4 != 0 || G < 2) return false;
+  const int nv4 = dim / 4;
+  if (nv4 % G != 0) return false;
+  out = vec_variant(G, nv4 / G);
+  return out.G != 0;
+}
+
+bool pick_variant(int dim, bool aligned, bool exact, Variant &out) {
+  if (aligned && !exact) {
+    const int G = preferred_lanes(dim);
+    for (int g = G; g <= 32; g *= 2)
+      if (pick_vector(dim, g, out)) return true;
+    for (int g = G / 2; g >= 2; g /= 2)
+      if (pick_vector(dim, g, out)) return true;
+  }
+  const int ns = (dim + 31) / 32;
+  for (int s = 1; s <= 16; s *= 2)
+    if (ns <= s) {
+      out = scalar_variant(s, exact);
+      return out.G != 0;
+    }
+  return false;
+}
+
+bool aligned16(const void *p, int dim) {
+  return (reinterpret_cast<uintptr_t>(p) & 15u) == 0 && dim % 4 == 0;
+}
+
+int grid_for(const void *sym, int G, int64_t max_groups, int64_t work_items, int *grid) {
+  int occ = 0;
+  GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym, kBlock, 0));
+  if (occ < 1) occ = 1;
+  const int64_t groups_per_block = kBlock / G;
+  const int64_t want = (int64_t)num_sms() * occ;
+  int64_t cap_groups = max_groups > 0 ? max_groups : INT64_MAX;
+  cap_groups = std::min(cap_groups, std::max<int64_t>(work_items, 1));
+  const int64_t need = (cap_groups + groups_per_block - 1) / groups_per_block;
+  *grid = (int)std::max<int64_t>(1, std::min(want, need));
+  return GB_OK;
+}
+
+}  // namespace
+}  // namespace tk
+}  // namespace gb
+
+using namespace gb;
+using namespace gb::tk;
+
+GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int32_t *adj,
+                               float *M, int dim, int n_neg, uint64_t seed, uint64_t rng_stream,
+                               int64_t pass_begin, int64_t n_passes, int64_t passes_per_epoch,
+                               const float *lr_per_epoch, unsigned flags, int64_t max_groups,
+                               int64_t *status, void *stream_handle) {
+  GB_REQUIRE(num_vertices >= 0 && dim >= 1 && n_neg >= 0, "gb_train_passes: bad sizes");
+  GB_REQUIRE(passes_per_epoch >= 1 && pass_begin >= 0 && n_passes >= 0,
+             "gb_train_passes: bad pass range");
+  GB_REQUIRE(xadj && M && lr_per_epoch && status, "gb_train_passes: null pointer");
+  if (num_vertices == 0 || n_passes == 0) return GB_OK;
+  const bool exact = flags & GB_TRAIN_EXACT;
+  Variant var;
+  GB_REQUIRE(pick_variant(dim, aligned16(M, dim), exact, var),
+             "gb_train_passes: dim %d unsupported", dim);
+  PassArgs a{num_vertices, xadj, adj, M, dim, n_neg, seed, rng_stream, pass_begin, n_passes,
+             passes_per_epoch, lr_per_epoch, (flags & GB_TRAIN_REUSE) != 0,
+             exact ? 1 : max_groups, status};
+  int grid = 1;
+  if (!exact) {
+    int rc = grid_for((const void *)var.pass, var.G, max_groups, num_vertices, &grid);
+    if (rc) return rc;
+  }
+  var.pass<<<grid, kBlock, 0, as_stream(stream_handle)>>>(a);
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
+GB_API int gb_train_pool_side(float *Msrc, float *Mtgt, int dim, const int32_t *targets,
+                                  int64_t n_src, int B, int64_t lo_t, int64_t n_t, int n_neg,
+                                  double lr, uint64_t seed, uint64_t side, const int64_t *xadj,
+                                  const int32_t *adj, int64_t lo_s, uint64_t pool_side,
+                                  unsigned flags, int64_t max_groups, int64_t *status,
+                                  void *stream_handle) {
+  GB_REQUIRE(dim >= 1 && B >= 1 && n_neg >= 0 && n_src >= 0 && n_t >= 0,
+             "gb_train_pool_side: bad sizes");
+  GB_REQUIRE(Msrc && Mtgt && status, "gb_train_pool_side: null pointer");
+  GB_REQUIRE(targets || (xadj && adj), "gb_train_pool_side: need targets or a CSR");
+  if (n_src == 0 || n_t == 0) return GB_OK;
+  const bool exact = flags & GB_TRAIN_EXACT;
+  Variant var;
+  GB_REQUIRE(pick_variant(dim, aligned16(Msrc, dim) && aligned16(Mtgt, dim), exact, var),
+             "gb_train_pool_side: dim %d unsupported", dim);
+  PoolArgs a{Msrc, Mtgt, dim, targets, n_src, B, lo_t, n_t, n_neg, lr, seed, side, xadj, adj,
+             lo_s, pool_side, (flags & GB_TRAIN_REUSE) != 0, exact ? 1 : max_groups, status};
+  int grid = 1;
+  if (!exact) {
+    int rc = grid_for((const void *)var.pool, var.G, max_groups, n_src, &grid);
+    if (rc) return rc;
+  }
+  var.pool<<<grid, kBlock, 0, as_stream(stream_handle)>>>(a);
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
+GB_API int gb_nonfinite_scan(const float *M, int64_t count, int64_t epoch, int64_t *status,
+                                 void *stream_handle) {
+  GB_REQUIRE(count >= 0 && status, "gb_nonfinite_scan: bad args");
+  if (count == 0) return GB_OK;
+  const int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)num_sms() * 8);
+  nonfinite_scan_kernel<<<(int)blocks, 256, 0, as_stream(stream_handle)>>>(M, count, epoch,
+                                                                           status);
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}

@@ -1,0 +1,447 @@
+// VERSE/NCE training kernels (templates; instantiated per row layout in
+// train_v*.cu): the in-memory vertex pass (trainer.py:184-207)
+// and the partitioned pool side (bigtrain.py:215-238), sm_100a.
+//
+// Work decomposition: a "group" of G lanes of one warp owns one source vertex
+// at a time.  The source row lives in the group's registers for all of its
+// 1+n_neg (resp. B*(1+n_neg)) chained updates and is written back once; the
+// sample rows of a chunk of CH samples are gathered up front (their ids are a
+// pure function of the counter-based key, so only the positive waits on the
+// xadj->adj chain), updated in registers in the reference's order, and
+// written back right after their update (Hogwild).  Repeated samples inside a
+// chunk are forwarded in registers; a sample equal to the source uses the
+// register copy of the source with the reference's aliasing rule.
+//
+// Arithmetic is the reference's: fp64 dot of fp32 values (products are exact
+// in fp64, so only the summation order can differ -- serial in EXACT mode),
+// fp64 clamp/sigmoid, score rounded to fp32, unfused fp32 row updates.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <climits>
+
+#include "common.cuh"
+
+namespace gb {
+namespace tk {
+
+constexpr int kChunk = 4;  // sample rows gathered per step
+constexpr int kBlock = 256;
+constexpr double kClamp = 10.0;  // SIGMOID_CLAMP, trainer.py:35
+
+// ---------------------------------------------------------------------------
+// Row fragments.  Row::load/store move one embedding row between global
+// memory and the registers of the G lanes of a group.
+// ---------------------------------------------------------------------------
+
+// dim == 4*G*NV: lane l holds float4 number k*G + l (k < NV); fully coalesced
+// 16-byte accesses, one 128-byte line per 8 lanes.
+template <int G_, int NV>
+struct VecRow {
+  static constexpr int G = G_;
+  static constexpr int E = 4 * NV;
+  float x[E];
+  __device__ __forceinline__ static bool valid(int, int, int) { return true; }
+  __device__ __forceinline__ void load(const float *row, int gl, int) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float4 v = __ldcg(reinterpret_cast<const float4 *>(row) + k * G + gl);
+      x[4 * k + 0] = v.x;
+      x[4 * k + 1] = v.y;
+      x[4 * k + 2] = v.z;
+      x[4 * k + 3] = v.w;
+    }
+  }
+  __device__ __forceinline__ void store(float *row, int gl, int) const {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float4 v = make_float4(x[4 * k + 0], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
+      __stcg(reinterpret_cast<float4 *>(row) + k * G + gl, v);
+    }
+  }
+  // Serial dot in ascending element order (the reference's loop order,
+  // trainer.py:122-123): element t = 4*(k*G + l) + c.
+  __device__ __forceinline__ static double serial_dot(const VecRow &a, const VecRow &b,
+                                                      unsigned gmask, int, int) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double p[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        p[c] = __dmul_rn((double)a.x[4 * k + c], (double)b.x[4 * k + c]);
+#pragma unroll 1
+      for (int src = 0; src < G; ++src) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc = __dadd_rn(acc, __shfl_sync(gmask, p[c], src, G));
+      }
+    }
+    return acc;
+  }
+};
+
+// Any dim <= 32*NS: G = 32, lane l holds elements k*32 + l (k < NS).
+template <int NS>
+struct ScalarRow {
+  static constexpr int G = 32;
+  static constexpr int E = NS;
+  float x[E];
+  __device__ __forceinline__ static bool valid(int k, int gl, int dim) { return k * 32 + gl < dim; }
+  __device__ __forceinline__ void load(const float *row, int gl, int dim) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) x[k] = valid(k, gl, dim) ? __ldcg(row + k * 32 + gl) : 0.0f;
+  }
+  __device__ __forceinline__ void store(float *row, int gl, int dim) const {
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+      if (valid(k, gl, dim)) __stcg(row + k * 32 + gl, x[k]);
+  }
+  __device__ __forceinline__ static double serial_dot(const ScalarRow &a, const ScalarRow &b,
+                                                      unsigned gmask, int gl, int dim) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      double p = __dmul_rn((double)a.x[k], (double)b.x[k]);
+#pragma unroll 1
+      for (int src = 0; src < 32; ++src) {
+        double q = __shfl_sync(gmask, p, src, 32);
+        if (k * 32 + src < dim) acc = __dadd_rn(acc, q);
+      }
+    }
+    return acc;
+  }
+};
+
+// fp64 dot of two fp32 fragments.  Tree mode: per-lane partial sums of exact
+// products then an xor butterfly (identical result on every lane).
+template <class Row, bool EXACT>
+__device__ __forceinline__ double row_dot(const Row &a, const Row &b, unsigned gmask, int gl,
+                                          int dim) {
+  if (EXACT) return Row::serial_dot(a, b, gmask, gl, dim);
+  double part = 0.0;
+#pragma unroll
+  for (int k = 0; k < Row::E; ++k)
+    if (Row::valid(k, gl, dim)) part = __fma_rn((double)a.x[k], (double)b.x[k], part);
+#pragma unroll
+  for (int off = Row::G / 2; off > 0; off >>= 1)
+    part = __dadd_rn(part, __shfl_xor_sync(gmask, part, off, Row::G));
+  return part;
+}
+
+// score = f32((b - sigmoid(clamp(acc))) * lr)   (trainer.py:124-130)
+__device__ __forceinline__ float nce_score(double acc, double b, double lr, bool &bad) {
+  bad |= !isfinite(acc);
+  if (acc > kClamp)
+    acc = kClamp;
+  else if (acc < -kClamp)
+    acc = -kClamp;
+  double sig = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-acc)));
+  return __double2float_rn(__dmul_rn(__dsub_rn(b, sig), lr));
+}
+
+// Update of a distinct sample row (trainer.py:131-140).
+template <class Row>
+__device__ __forceinline__ void update_pair(Row &S, Row &R, float sc, bool reuse) {
+  if (reuse) {
+#pragma unroll
+    for (int k = 0; k < Row::E; ++k) S.x[k] = __fadd_rn(S.x[k], __fmul_rn(R.x[k], sc));
+#pragma unroll
+    for (int k = 0; k < Row::E; ++k) R.x[k] = __fadd_rn(R.x[k], __fmul_rn(S.x[k], sc));
+  } else {
+#pragma unroll
+    for (int k = 0; k < Row::E; ++k) {
+      float vo = S.x[k];
+      S.x[k] = __fadd_rn(vo, __fmul_rn(R.x[k], sc));
+      R.x[k] = __fadd_rn(R.x[k], __fmul_rn(vo, sc));
+    }
+  }
+}
+
+// Self-sample (s == v).  In-place rule of the single-array kernel
+// (_train_pass passes M twice): M[v] = fl(fl(vo + vo*sc) + vo*sc).  Load-once
+// rule of the two-array pool kernel on a diagonal pair (numba marks the two
+// array arguments noalias, bigtrain.py:234): M[i] = fl(vo + vo*sc).  With
+// reuse both paths run the two whole-row loops in sequence.
+template <class Row>
+__device__ __forceinline__ void update_self(Row &S, float sc, bool reuse, bool load_once) {
+  if (reuse) {
+#pragma unroll
+    for (int k = 0; k < Row::E; ++k) {
+      float n1 = __fadd_rn(S.x[k], __fmul_rn(S.x[k], sc));
+      S.x[k] = __fadd_rn(n1, __fmul_rn(n1, sc));
+    }
+  } else if (load_once) {
+#pragma unroll
+    for (int k = 0; k < Row::E; ++k) S.x[k] = __fadd_rn(S.x[k], __fmul_rn(S.x[k], sc));
+  } else {
+#pragma unroll
+    for (int k = 0; k < Row::E; ++k) {
+      float vo = S.x[k];
+      float d = __fmul_rn(vo, sc);
+      S.x[k] = __fadd_rn(__fadd_rn(vo, d), d);
+    }
+  }
+}
+
+struct GroupCtx {
+  int gl;          // lane inside the group
+  unsigned gmask;  // lanes of this group
+};
+
+template <class Row>
+__device__ __forceinline__ GroupCtx group_ctx() {
+  GroupCtx c;
+  const int lane = threadIdx.x & 31;
+  c.gl = lane % Row::G;
+  c.gmask = Row::G == 32 ? 0xffffffffu : (((1u << Row::G) - 1u) << (lane / Row::G * Row::G));
+  return c;
+}
+
+// Runs one chunk of up to kChunk samples against the register-resident
+// source S.  ids[j] < 0 marks an unused slot.  Sample rows are gathered first,
+// then updated in order with forwarding, and stored immediately.
+template <class Row, bool EXACT>
+__device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int64_t (&ids)[kChunk],
+                                          const double (&bs)[kChunk], float *__restrict__ Mtgt,
+                                          int dim, double lr, bool reuse, bool self_possible,
+                                          bool load_once, const GroupCtx &g, bool &bad) {
+  Row R[kChunk];
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j)
+    if (ids[j] >= 0 && !(self_possible && ids[j] == src_row))
+      R[j].load(Mtgt + ids[j] * (int64_t)dim, g.gl, dim);
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) {
+    const int64_t s = ids[j];
+    if (s < 0) continue;
+    if (self_possible && s == src_row) {
+      double acc = row_dot<Row, EXACT>(S, S, g.gmask, g.gl, dim);
+      float sc = nce_score(acc, bs[j], lr, bad);
+      update_self(S, sc, reuse, load_once);
+      continue;
+    }
+    double acc = row_dot<Row, EXACT>(S, R[j], g.gmask, g.gl, dim);
+    float sc = nce_score(acc, bs[j], lr, bad);
+    update_pair(S, R[j], sc, reuse);
+#pragma unroll
+    for (int jj = j + 1; jj < kChunk; ++jj)
+      if (ids[jj] == s) R[jj] = R[j];
+    R[j].store(Mtgt + s * (int64_t)dim, g.gl, dim);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// In-memory passes (trainer.py:184-207).
+// ---------------------------------------------------------------------------
+struct PassArgs {
+  int64_t V;
+  const int64_t *__restrict__ xadj;
+  const int32_t *__restrict__ adj;
+  float *M;
+  int dim;
+  int n_neg;
+  uint64_t seed;
+  uint64_t stream;
+  int64_t pass_begin;
+  int64_t n_passes;
+  int64_t ppe;
+  const float *__restrict__ lr;
+  bool reuse;
+  int64_t max_groups;
+  int64_t *status;
+};
+
+template <class Row, bool EXACT>
+__global__ void __launch_bounds__(kBlock) train_passes_kernel(PassArgs a) {
+  const GroupCtx g = group_ctx<Row>();
+  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / Row::G;
+  const int64_t ngroups =
+      min((int64_t)gridDim.x * blockDim.x / Row::G, a.max_groups > 0 ? a.max_groups : INT64_MAX);
+  if (gid >= ngroups) return;  // whole groups leave together
+  bool bad = false;
+  int64_t first_bad = INT64_MAX;
+  const int nsamp = 1 + a.n_neg;
+
+  for (int64_t p = a.pass_begin; p < a.pass_begin + a.n_passes; ++p) {
+    const int64_t epoch = p / a.ppe;
+    const double lr = (double)a.lr[epoch];
+    for (int64_t v = gid; v < a.V; v += ngroups) {
+      const int64_t x0 = __ldg(a.xadj + v);
+      const int64_t deg = __ldg(a.xadj + v + 1) - x0;
+      if (deg == 0) continue;  // isolated sources are skipped (trainer.py:198-200)
+      const uint64_t key = stream_key(a.seed, a.stream, (uint64_t)p, (uint64_t)v);
+      Row S;
+      S.load(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+      bool bad_src = false;
+      for (int c0 = 0; c0 < nsamp; c0 += kChunk) {
+        int64_t ids[kChunk];
+        double bs[kChunk];
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          const int idx = c0 + j;
+          if (idx >= nsamp) {
+            ids[j] = -1;
+          } else if (idx == 0) {  // positive: uniform neighbour (trainer.py:203)
+            ids[j] = __ldg(a.adj + x0 + draw_below(key, 0, deg));
+          } else {  // negatives: uniform over V (trainer.py:205-206)
+            ids[j] = draw_below(key, (uint64_t)idx, a.V);
+          }
+          bs[j] = idx == 0 ? 1.0 : 0.0;
+        }
+        run_chunk<Row, EXACT>(S, v, ids, bs, a.M, a.dim, lr, a.reuse, true, false, g, bad_src);
+      }
+      S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+      if (bad_src) {
+        bad = true;
+        first_bad = min(first_bad, epoch);
+      }
+    }
+  }
+  if (bad && g.gl == 0) {
+    atomicOr(reinterpret_cast<unsigned long long *>(a.status), 1ull);
+    atomicMin(reinterpret_cast<long long *>(a.status + 1), (long long)first_bad);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pool side (bigtrain.py:215-238), optionally drawing the pool on the fly
+// (bigtrain.py:164-196) from the device CSR.
+// ---------------------------------------------------------------------------
+struct PoolArgs {
+  float *Msrc;
+  float *Mtgt;
+  int dim;
+  const int32_t *__restrict__ targets;
+  int64_t n_src;
+  int B;
+  int64_t lo_t;
+  int64_t n_t;
+  int n_neg;
+  double lr;
+  uint64_t seed;
+  uint64_t side;
+  const int64_t *__restrict__ xadj;
+  const int32_t *__restrict__ adj;
+  int64_t lo_s;
+  uint64_t pool_side;
+  bool reuse;
+  int64_t max_groups;
+  int64_t *status;
+};
+
+// lower_bound over adj[lo, hi) (rows are sorted ascending).
+__device__ __forceinline__ int64_t lower_bound_adj(const int32_t *__restrict__ adj, int64_t lo,
+                                                   int64_t hi, int64_t x) {
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)__ldg(adj + mid) < x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+template <class Row, bool EXACT>
+__global__ void __launch_bounds__(kBlock) train_pool_kernel(PoolArgs a) {
+  const GroupCtx g = group_ctx<Row>();
+  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / Row::G;
+  const int64_t ngroups =
+      min((int64_t)gridDim.x * blockDim.x / Row::G, a.max_groups > 0 ? a.max_groups : INT64_MAX);
+  if (gid >= ngroups) return;
+  const bool diagonal = a.Msrc == a.Mtgt;
+  const int per_t = 1 + a.n_neg;
+  const int64_t total = (int64_t)a.B * per_t;
+  bool bad = false;
+  unsigned long long pos_count = 0;
+
+  for (int64_t i = gid; i < a.n_src; i += ngroups) {
+    // pool side of this source: either the materialized row or the fused draw
+    int64_t first = 0, cnt = 0;
+    uint64_t pkey = 0;
+    if (a.targets == nullptr) {
+      const int64_t v = a.lo_s + i;
+      const int64_t e0 = __ldg(a.xadj + v), e1 = __ldg(a.xadj + v + 1);
+      first = lower_bound_adj(a.adj, e0, e1, a.lo_t);
+      cnt = lower_bound_adj(a.adj, first, e1, a.lo_t + a.n_t) - first;
+      if (cnt == 0) continue;  // every slot is -1
+      pkey = stream_key(a.seed, a.pool_side, 0, (uint64_t)v);
+    }
+    const uint64_t key = stream_key(a.seed, a.side, 1, (uint64_t)i);
+    Row S;
+    bool loaded = false;
+    for (int64_t c0 = 0; c0 < total; c0 += kChunk) {
+      int64_t ids[kChunk];
+      double bs[kChunk];
+      bool any = false;
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        const int64_t idx = c0 + j;
+        ids[j] = -1;
+        bs[j] = 0.0;
+        if (idx >= total) continue;
+        const int64_t t = idx / per_t;
+        const int q = (int)(idx - t * per_t);
+        int64_t tgt;
+        if (a.targets != nullptr)
+          tgt = __ldg(a.targets + i * a.B + t);
+        else
+          tgt = __ldg(a.adj + first + draw_below(pkey, (uint64_t)t, cnt));
+        if (tgt < 0) continue;  // absent slot: no positive, no negatives
+        if (q == 0) {
+          ids[j] = tgt - a.lo_t;
+          bs[j] = 1.0;
+        } else {
+          ids[j] = draw_below(key, (uint64_t)(t * a.n_neg + (q - 1)), a.n_t);
+        }
+        any = true;
+      }
+      if (!any) continue;
+      if (!loaded) {
+        S.load(a.Msrc + i * (int64_t)a.dim, g.gl, a.dim);
+        loaded = true;
+      }
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) pos_count += (ids[j] >= 0 && bs[j] == 1.0) ? 1 : 0;
+      run_chunk<Row, EXACT>(S, i, ids, bs, a.Mtgt, a.dim, a.lr, a.reuse, diagonal, true, g, bad);
+    }
+    if (loaded) S.store(a.Msrc + i * (int64_t)a.dim, g.gl, a.dim);
+  }
+  if (g.gl == 0) {
+    if (pos_count) atomicAdd(reinterpret_cast<unsigned long long *>(a.status + 2), pos_count);
+    if (bad) {
+      atomicOr(reinterpret_cast<unsigned long long *>(a.status), 1ull);
+      atomicMin(reinterpret_cast<long long *>(a.status + 1), 0ll);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Per-layout kernel table.
+// ---------------------------------------------------------------------------
+using PassFn = void (*)(PassArgs);
+using PoolFn = void (*)(PoolArgs);
+
+struct Variant {
+  int G = 0;
+  PassFn pass = nullptr;
+  PoolFn pool = nullptr;
+};
+
+template <class Row, bool EXACT>
+Variant make_variant() {
+  Variant v;
+  v.G = Row::G;
+  v.pass = train_passes_kernel<Row, EXACT>;
+  v.pool = train_pool_kernel<Row, EXACT>;
+  return v;
+}
+
+// Fast layouts (tree dot): VecRow<G, NV>, dim = 4*G*NV.
+Variant vec_variant(int G, int NV);  // returns G == 0 if not instantiated
+// Any-dim layouts (ScalarRow<NS>, dim <= 32*NS); exact = serial dot.
+Variant scalar_variant(int NS, bool exact);
+
+}  // namespace tk
+}  // namespace gb
