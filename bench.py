@@ -1,0 +1,330 @@
+"""Benchmark: the VERSE/NCE training pass on the C2 workload.
+
+Workload (BASELINE.json configs[1], SURVEY.md 8(d) "C2"): single-level
+embedding-kernel microbench on a synthetic R-MAT graph, scale 20 (1,048,576
+ids, all kept), 16,777,216 sampled edges, d=128, 3 negatives,
+init_embedding(V, 128, seed=1), lr 0.035 constant.  One step = one vertex
+pass over every non-isolated source = one launch of the training kernel.
+
+Metric: sample-updates/s (TrainStats definition, trainer.py:238-240: passes x
+non-isolated x (1+n_s)), with the kernel's achieved HBM GB/s against the
+measured copy bandwidth (algorithmic bytes 8d(2+n_s)+12 per source).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1 (torchrun, one rank per GPU): each rank trains its own replica of the
+workload (weak scaling, no data-path collective -- the in-memory pass does
+not shard).  `--impl reference` times the reference's CPU path
+(the oracle's C restatement of _train_pass, all host threads) on the same
+workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SCALE, SAMPLES, DIM, NNEG, SEED, LR = 20, 1 << 24, 128, 3, 7, 0.035
+METRIC = "sample-updates/sec"
+UNIT = "updates/s"
+
+
+def workload_config(extra=None):
+    cfg = {"workload": "C2 single-level VERSE pass: R-MAT scale 20 (2^20 ids, 2^24 sampled "
+                       "edges, Graph500 a,b,c=0.57,0.19,0.19), d=128, n_neg=3",
+           "scale": SCALE, "sampled_edges": SAMPLES, "dim": DIM, "negatives": NNEG,
+           "rmat_seed": SEED, "lr": LR, "step": "one vertex pass (1 kernel launch)",
+           "l2": "inputs larger than L2 (embedding matrix 512 MiB > 126 MB L2), no flush"}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+def bytes_per_source(dim=DIM, n_neg=NNEG):
+    return 8 * dim * (2 + n_neg) + 12
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "train_kernel_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clock/throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_init():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def cpu_baseline(xadj, adj, seconds=12.0, warm=1):
+    """Oracle C restatement of _train_pass (Hogwild, all host threads) on the
+    same graph: bounded sample of whole passes."""
+    from oracle import oracle as orc
+    threads = orc.max_threads()
+    V = len(xadj) - 1
+    M = orc.init_embedding(V, DIM, 1)
+    non_iso = int((np.diff(xadj) > 0).sum())
+    for p in range(warm):
+        orc.train_pass(xadj, adj, M, LR, NNEG, 1, 0, p, nthreads=threads)
+    passes, t0 = 0, time.perf_counter()
+    while True:
+        orc.train_pass(xadj, adj, M, LR, NNEG, 1, 0, warm + passes, nthreads=threads)
+        passes += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    upd = passes * non_iso * (1 + NNEG)
+    return {"value": upd / el, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{passes} full C2 passes ({upd} updates) of oracle/gosh_oracle.c "
+                      f"or_train_pass, {threads} threads, {el:.1f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+    xadj, adj = orc.rmat_graph(SCALE, SAMPLES, SEED)
+    threads = orc.max_threads()
+    V = len(xadj) - 1
+    M = orc.init_embedding(V, DIM, 1)
+    non_iso = int((np.diff(xadj) > 0).sum())
+    for p in range(args.warmup):
+        orc.train_pass(xadj, adj, M, LR, NNEG, 1, 0, p, nthreads=threads)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        orc.train_pass(xadj, adj, M, LR, NNEG, 1, 0, args.warmup + k, nthreads=threads)
+    el = time.perf_counter() - t0
+    value = args.steps * non_iso * (1 + NNEG) / el
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": el * 1000.0 / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows / f64 dot",
+        "data": "synthetic R-MAT (CPU generator, bit-identical to the GPU one)",
+        "config": workload_config({"parallelism": "host threads"}),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} timed full C2 passes after {args.warmup} "
+                                   f"warm-up passes, oracle/gosh_oracle.c or_train_pass"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_init()
+    import paper_2008_12336_b200 as gb
+    from paper_2008_12336_b200 import _lib
+    dev = torch.device("cuda", local)
+
+    t_build = time.perf_counter()
+    G = gb.rmat_graph(SCALE, SAMPLES, SEED)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t_build
+    xadj, adj = G.device_csr()
+    V = G.num_vertices
+    non_iso = int((xadj[1:] > xadj[:-1]).sum().item())
+    M = torch.from_numpy(gb.init_embedding(V, DIM, 1)).to(dev)
+    lrs = torch.tensor([np.float32(LR)], dtype=torch.float32, device=dev)
+    status = _lib.new_status()
+    stream = torch.cuda.current_stream()
+    cap = gb.trainer.inflight_cap(gb.TrainConfig(dim=DIM), V)
+
+    def launch(p):
+        _lib.call("gb_train_passes", V, _lib.ptr(xadj), _lib.ptr(adj), _lib.ptr(M), DIM, NNEG,
+                  1, 0, p, 1, 1 << 40, _lib.ptr(lrs), 0, cap, _lib.ptr(status),
+                  stream.cuda_stream)
+
+    for p in range(args.warmup):
+        launch(p)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for k in range(args.steps):
+            starts[k].record(stream)
+            launch(args.warmup + k)
+            ends[k].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+    total_ms = t0.elapsed_time(t1)
+    kern_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    upd_per_step = non_iso * (1 + NNEG)
+    value = world * upd_per_step / (ms_per_step / 1000.0)
+    if int(status[0].item()):
+        raise FloatingPointError("non-finite embedding during the benchmark")
+
+    # e2e through the public API with host buffers: one train_level call per
+    # step (one edge-scaled epoch = ceil(E/V) passes), M copied in from pinned
+    # host memory and back every step.
+    M_host = torch.from_numpy(gb.init_embedding(V, DIM, 1)).pin_memory()
+    cfg = gb.TrainConfig(dim=DIM, negative_samples=NNEG, seed=1, learning_rate=LR,
+                         epoch_unit="edge-scaled")
+    e2e_steps = max(2, min(args.steps // 10, 5))
+    gb.train_level(G, M_host, cfg, 1)  # warm-up
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    te = time.perf_counter()
+    e2e_upd = 0
+    for _ in range(e2e_steps):
+        st = gb.train_level(G, M_host, cfg, 1)
+        e2e_upd += st.updates
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - te
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * e2e_upd / e2e_s
+    ppe = gb.trainer.passes_per_epoch(G, cfg)
+
+    bps = bytes_per_source()
+    achieved = non_iso * bps / (kern_ms / 1000.0) / 1e9
+    peak, peak_src = measured_peak()
+    traffic = ncu_traffic()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows / f64 dot",
+        "data": "synthetic R-MAT generated on device (seeded, Graph500 parameters)",
+        "config": workload_config({
+            "vertices": V, "non_isolated_sources": non_iso, "arcs": G.num_edges,
+            "parallelism": "replicas" if world > 1 else "single GPU",
+            "inflight_groups_cap": cap, "graph_build_s": round(build_s, 3)}),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": non_iso * bps,
+                     "bytes_per_source": bps, "kernel_ms": kern_ms, "peak_source": peak_src},
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": V * DIM * 4, "d2h_bytes_per_step": V * DIM * 4,
+                "step": f"train_level(g, M_pinned_host, edge-scaled, e_i=1): {ppe} passes + "
+                        f"M in/out", "steps": e2e_steps},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(xadj.cpu().numpy(), adj[: G.num_edges].cpu().numpy(),
+                                            seconds=args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -145,6 +145,16 @@ int gb_train_passes(int64_t num_vertices, const int64_t *xadj,
                     const float *lr_per_epoch, unsigned flags,
                     int64_t max_groups, int64_t *status, void *stream_handle);
 
+/* Fixed sample lists (update_embedding, trainer.py:137-142, generalized):
+ * source src[i] is updated against samples[i*k + j] for j = 0..k-1 in order
+ * (-1 skips a slot) with label labels[j] (1 positive, 0 negative), single-
+ * array semantics, lr as float64.  Different sources run concurrently
+ * (Hogwild) unless GB_TRAIN_EXACT, which applies the lists in index order. */
+int gb_apply_sample_lists(float *M, int dim, int64_t n_src, const int64_t *src,
+                          int k, const int64_t *samples, const int8_t *labels,
+                          double lr, unsigned flags, int64_t max_groups,
+                          int64_t *status, void *stream_handle);
+
 /* Full-matrix non-finite scan (fallback half of trainer.py:236-237; rows no
  * update touched).  Sets status[0] and status[1]=epoch when any entry is
  * NaN/Inf. */

@@ -1,0 +1,136 @@
+"""ctypes binding of the C ABI in include/gosh_b200.h (libgosh_b200.so).
+
+This is the reference-side binding a maintainer would add: every entry point
+takes plain device pointers, sizes and a cudaStream_t.  Device buffers are
+torch CUDA tensors (torch is plumbing here: allocation, streams, copies);
+the compute is the library's sm_100a kernels.  There is no fallback: a
+missing library or a missing GPU raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from .errors import MlembedError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgosh_b200.so")
+
+GB_OK = 0
+GB_E_INVALID = -1
+GB_TRAIN_REUSE = 1
+GB_TRAIN_EXACT = 2
+GB_CSR_DROP_SELF = 1
+GB_CSR_SYMMETRIZE = 2
+STATUS_WORDS = 4
+
+_p, _i64, _u64, _int, _dbl, _sz = C.c_void_p, C.c_int64, C.c_uint64, C.c_int, C.c_double, C.c_size_t
+_pi64 = C.POINTER(C.c_int64)
+_pint = C.POINTER(C.c_int)
+_psz = C.POINTER(C.c_size_t)
+
+SIGNATURES = {
+    "gb_last_error": (C.c_char_p, []),
+    "gb_version": (_int, []),
+    "gb_device_info": (_int, [_int, _pint, _pint]),
+    "gb_rng_draw_below": (_int, [_u64, _u64, _u64, _u64, _u64, _i64, _i64, _p, _p]),
+    "gb_csr_build_workspace": (_int, [_i64, _i64, C.c_uint, _psz]),
+    "gb_csr_build": (_int, [_i64, _p, _p, _i64, C.c_uint, _p, _p, _pi64, _p, _sz, _p]),
+    "gb_csr_densify_workspace": (_int, [_i64, _psz]),
+    "gb_csr_densify": (_int, [_i64, _i64, _p, _p, _p, _p, _p, _p, _pi64, _p, _sz, _p]),
+    "gb_rmat_permutation_workspace": (_int, [_int, _psz]),
+    "gb_rmat_permutation": (_int, [_int, _u64, _p, _p, _sz, _p]),
+    "gb_rmat_edges": (_int, [_int, _i64, _dbl, _dbl, _dbl, _u64, _p, _p, _p, _p]),
+    "gb_degree_order_workspace": (_int, [_i64, _psz]),
+    "gb_degree_order": (_int, [_i64, _p, _p, _p, _sz, _p]),
+    "gb_collapse_workspace": (_int, [_i64, _psz]),
+    "gb_collapse": (_int, [_i64, _p, _p, _p, _p, _dbl, _p, _pi64, _pint, _p, _sz, _p]),
+    "gb_coarse_csr_workspace": (_int, [_i64, _i64, _i64, _psz]),
+    "gb_coarse_csr": (_int, [_i64, _i64, _p, _p, _p, _i64, _p, _p, _pi64, _p, _sz, _p]),
+    "gb_expand": (_int, [_p, _i64, _int, _p, _i64, _p, _p]),
+    "gb_train_passes": (_int, [_i64, _p, _p, _p, _int, _int, _u64, _u64, _i64, _i64, _i64, _p,
+                               C.c_uint, _i64, _p, _p]),
+    "gb_apply_sample_lists": (_int, [_p, _int, _i64, _p, _int, _p, _p, _dbl, C.c_uint, _i64, _p,
+                                     _p]),
+    "gb_nonfinite_scan": (_int, [_p, _i64, _i64, _p, _p]),
+    "gb_fill_pool_side": (_int, [_p, _p, _i64, _i64, _i64, _i64, _int, _u64, _u64, _p, _p]),
+    "gb_train_pool_side": (_int, [_p, _p, _int, _p, _i64, _int, _i64, _i64, _int, _dbl, _u64,
+                                  _u64, _p, _p, _i64, _u64, C.c_uint, _i64, _p, _p]),
+}
+
+_lib = None
+
+
+class NativeLibraryError(MlembedError, RuntimeError):
+    """The CUDA library is missing or failed."""
+
+
+def load():
+    """Load libgosh_b200.so (no GPU needed to load; every compute call needs one)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeLibraryError(
+                f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; "
+                f"g.build()'` (or `make lib`) -- there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def u64(x: int) -> int:
+    return int(x) & 0xFFFFFFFFFFFFFFFF
+
+
+def check(rc: int, what: str) -> None:
+    if rc == GB_OK:
+        return
+    msg = load().gb_last_error().decode(errors="replace")
+    if rc == GB_E_INVALID:
+        raise ValueError(f"{what}: {msg}")
+    raise NativeLibraryError(f"{what} failed ({rc}): {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise NativeLibraryError("paper_2008_12336_b200 needs a CUDA device (B200); "
+                                 "there is no CPU path")
+    load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    assert t.is_cuda and t.is_contiguous(), "device buffers must be contiguous CUDA tensors"
+    return t.data_ptr()
+
+
+def workspace(query: str, *args) -> tuple[torch.Tensor, int]:
+    n = C.c_size_t(0)
+    call(query, *args, C.byref(n))
+    ws = torch.empty(max(int(n.value), 1), dtype=torch.uint8, device="cuda")
+    return ws, int(n.value)
+
+
+def new_status() -> torch.Tensor:
+    """[nonfinite flag, first bad epoch, positive updates, reserved]."""
+    return torch.tensor([0, 2**63 - 1, 0, 0], dtype=torch.int64, device="cuda")
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES)

@@ -1,0 +1,202 @@
+"""MultiEdgeCollapse coarsening on the GPU (reference: coarsen.py).
+
+The reference's deterministic path is the sequential greedy `_collapse_seq`
+(coarsen.py:98-114); its parallel CAS collapse is run-dependent
+(coarsen.py:117-156).  Here both entry points run the same deterministic
+device algorithm: a vertex is a hub iff none of its
+lower-rank "H-neighbours" is a hub, and a member joins its minimum-rank hub
+H-neighbour -- decided in a few Gauss-Seidel rounds (gb_collapse), bit-equal
+to `_collapse_seq`.  The coarse graph is rebuilt by sorting mapped arcs
+(gb_coarse_csr).  Every level stays in HBM; host arrays materialize only on
+access.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ConfigError
+from .graph import Graph
+
+STALL_RATIO = 0.99  # coarsen.py:33
+
+
+class Mapping:
+    """Cluster assignment of one step: map[v] = cluster of v in the next
+    level, dense in [0, num_clusters) (coarsen.py:36-50).  Backed by a device
+    tensor when produced on the GPU."""
+
+    def __init__(self, map: np.ndarray | None = None, num_clusters: int = 0, *,
+                 map_dev: torch.Tensor | None = None):
+        if map is None and map_dev is None:
+            raise ValueError("Mapping needs a host or device map")
+        self._map = None if map is None else np.asarray(map)
+        self._map_dev = map_dev
+        self.num_clusters = int(num_clusters)
+
+    @property
+    def map(self) -> np.ndarray:
+        if self._map is None:
+            self._map = self._map_dev.cpu().numpy()
+        return self._map
+
+    @map.setter
+    def map(self, value) -> None:
+        self._map = np.asarray(value)
+        self._map_dev = None
+
+    def device_map(self) -> torch.Tensor:
+        _lib.require_cuda()
+        if self._map_dev is None:
+            self._map_dev = torch.from_numpy(np.ascontiguousarray(self._map, np.int32)).cuda()
+        return self._map_dev
+
+    def validate(self) -> None:
+        m = self.map
+        if m.shape[0] == 0:
+            raise ValueError("empty mapping")
+        if m.min() < 0 or m.max() >= self.num_clusters:
+            raise ValueError("cluster id out of range")
+        if np.bincount(m, minlength=self.num_clusters).min() < 1:
+            raise ValueError("mapping not surjective")
+
+    def __repr__(self) -> str:
+        return f"Mapping(num_clusters={self.num_clusters}, rows={self.rows})"
+
+    @property
+    def rows(self) -> int:
+        return int(self._map_dev.numel() if self._map_dev is not None else self._map.shape[0])
+
+
+@dataclass
+class Hierarchy:
+    """graphs[0] is the input, graphs[-1] the coarsest level; mappings[i]
+    sends level i to level i+1 (coarsen.py:53-66)."""
+
+    graphs: list[Graph]
+    mappings: list[Mapping]
+    stalled: bool = False
+    level_ms: list[float] = field(default_factory=list)
+    rounds: list[int] = field(default_factory=list)
+
+    @property
+    def depth(self) -> int:
+        return len(self.graphs)
+
+
+def _in_csr(g: Graph) -> tuple[torch.Tensor, torch.Tensor]:
+    """In-arc CSR: the graph itself when undirected, its transpose otherwise."""
+    xadj, adj = g.device_csr()
+    if not g.directed:
+        return xadj, adj
+    cached = getattr(g, "_transpose", None)
+    if cached is None:
+        from .graph import _csr_device
+        src = torch.repeat_interleave(torch.arange(g.num_vertices, device="cuda"),
+                                      xadj[1:] - xadj[:-1])
+        t = _csr_device(g.num_vertices, adj[: g.num_edges].long(), src, 0, True)
+        cached = t.device_csr()
+        g._transpose = cached
+    return cached
+
+
+def _degree_order_dev(g: Graph) -> torch.Tensor:
+    xadj, _ = g.device_csr()
+    V = g.num_vertices
+    ws, wsb = _lib.workspace("gb_degree_order_workspace", V)
+    order = torch.empty(V, dtype=torch.int64, device="cuda")
+    _lib.call("gb_degree_order", V, _lib.ptr(xadj), _lib.ptr(order), _lib.ptr(ws), wsb,
+              _lib.stream())
+    return order
+
+
+def degree_order(g: Graph) -> np.ndarray:
+    """Vertex ids by nonincreasing degree, ties by ascending id
+    (coarsen.py:69-95); stable device radix sort."""
+    return _degree_order_dev(g).cpu().numpy()
+
+
+def _collapse_dev(g: Graph, order) -> tuple[Mapping, int]:
+    xadj, _ = g.device_csr()
+    in_x, in_a = _in_csr(g)
+    V = g.num_vertices
+    if isinstance(order, torch.Tensor):
+        order_t = order.to(device="cuda", dtype=torch.int64).contiguous()
+    else:
+        order_t = torch.from_numpy(np.ascontiguousarray(order, dtype=np.int64)).cuda()
+    delta = g.num_edges / g.num_vertices  # coarsen.py:161
+    ws, wsb = _lib.workspace("gb_collapse_workspace", V)
+    cmap = torch.empty(V, dtype=torch.int32, device="cuda")
+    nc = C.c_int64(0)
+    rounds = C.c_int(0)
+    _lib.call("gb_collapse", V, _lib.ptr(xadj), _lib.ptr(in_x), _lib.ptr(in_a),
+              _lib.ptr(order_t), float(delta), _lib.ptr(cmap), C.byref(nc), C.byref(rounds),
+              _lib.ptr(ws), wsb, _lib.stream())
+    return Mapping(num_clusters=int(nc.value), map_dev=cmap), int(rounds.value)
+
+
+def collapse_map(g: Graph, order) -> Mapping:
+    """Greedy hub collapse, equal to the reference's sequential pass
+    (coarsen.py:159-163) for the given order."""
+    return _collapse_dev(g, order)[0]
+
+
+def collapse_map_parallel(g: Graph, order, num_workers: int) -> Mapping:
+    """Reference signature of the parallel collapse (coarsen.py:166-179).  The
+    device collapse is already parallel and deterministic, so every worker
+    count returns the sequential result (which the reference guarantees only
+    for num_workers=1)."""
+    if num_workers < 1:
+        raise ConfigError("num_workers must be >= 1")
+    return collapse_map(g, order)
+
+
+def build_coarse_graph(g: Graph, m: Mapping, num_workers: int = 1) -> Graph:
+    """Contract g along m: clusters become vertices, parallel arcs merged,
+    self-loops dropped, rows sorted (coarsen.py:256-281)."""
+    xadj, adj = g.device_csr()
+    cmap = m.device_map()
+    V, E, nc = g.num_vertices, g.num_edges, m.num_clusters
+    ws, wsb = _lib.workspace("gb_coarse_csr_workspace", V, E, nc)
+    x2 = torch.empty(nc + 1, dtype=torch.int64, device="cuda")
+    a2 = torch.empty(max(E, 1), dtype=torch.int32, device="cuda")
+    ne = C.c_int64(0)
+    _lib.call("gb_coarse_csr", V, E, _lib.ptr(xadj), _lib.ptr(adj), _lib.ptr(cmap), nc,
+              _lib.ptr(x2), _lib.ptr(a2), C.byref(ne), _lib.ptr(ws), wsb, _lib.stream())
+    del ws
+    E2 = int(ne.value)
+    a2 = a2[:max(E2, 1)].clone()
+    return Graph(nc, E2, directed=g.directed, xadj_dev=x2, adj_dev=a2)
+
+
+def coarsen_all(g: Graph, threshold: int = 100, num_workers: int = 1) -> Hierarchy:
+    """order -> collapse -> contract until |V| <= threshold; a level keeping
+    more than 99% of the vertices is discarded and flags a stall
+    (coarsen.py:284-311).  num_workers is accepted for API parity."""
+    if threshold < 1:
+        raise ConfigError("threshold must be >= 1")
+    if num_workers < 1:
+        raise ConfigError("num_workers must be >= 1")
+    graphs, mappings, level_ms, rounds = [g], [], [], []
+    stalled = False
+    while graphs[-1].num_vertices > threshold:
+        cur = graphs[-1]
+        t0 = time.perf_counter()
+        order = _degree_order_dev(cur)
+        m, r = _collapse_dev(cur, order)
+        if m.num_clusters > STALL_RATIO * cur.num_vertices:
+            stalled = True
+            break
+        nxt = build_coarse_graph(cur, m)
+        torch.cuda.current_stream().synchronize()
+        level_ms.append((time.perf_counter() - t0) * 1000.0)
+        graphs.append(nxt)
+        mappings.append(m)
+        rounds.append(r)
+    return Hierarchy(graphs=graphs, mappings=mappings, stalled=stalled, level_ms=level_ms,
+                     rounds=rounds)

@@ -163,3 +163,63 @@ GB_API int gb_nonfinite_scan(const float *M, int64_t count, int64_t epoch, int64
   GB_CHECK_LAUNCH();
   return GB_OK;
 }
+
+GB_API int gb_apply_sample_lists(float *M, int dim, int64_t n_src, const int64_t *src, int k,
+                                 const int64_t *samples, const int8_t *labels, double lr,
+                                 unsigned flags, int64_t max_groups, int64_t *status,
+                                 void *stream_handle) {
+  GB_REQUIRE(M && dim >= 1 && n_src >= 0 && k >= 0 && status, "gb_apply_sample_lists: bad args");
+  GB_REQUIRE(n_src == 0 || (src && (k == 0 || (samples && labels))),
+             "gb_apply_sample_lists: null pointer");
+  if (n_src == 0) return GB_OK;
+  const bool exact = flags & GB_TRAIN_EXACT;
+  Variant var;
+  GB_REQUIRE(pick_variant(dim, aligned16(M, dim), exact, var),
+             "gb_apply_sample_lists: dim %d unsupported", dim);
+  ListArgs a{M, dim, n_src, src, k, samples, labels, lr, (flags & GB_TRAIN_REUSE) != 0,
+             exact ? 1 : max_groups, status};
+  int grid = 1;
+  if (!exact) {
+    int rc = grid_for((const void *)var.lists, var.G, max_groups, n_src, &grid);
+    if (rc) return rc;
+  }
+  var.lists<<<grid, kBlock, 0, as_stream(stream_handle)>>>(a);
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
+namespace gb {
+namespace tk {
+namespace {
+// _fill_pool_side (bigtrain.py:164-196): one thread per source vertex.
+__global__ void fill_pool_kernel(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
+                                 int64_t lo_s, int64_t hi_s, int64_t lo_t, int64_t hi_t, int B,
+                                 uint64_t seed, uint64_t side, int32_t *__restrict__ out) {
+  for (int64_t v = lo_s + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < hi_s;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e1 = xadj[v + 1];
+    const int64_t first = lower_bound_adj(adj, xadj[v], e1, lo_t);
+    const int64_t cnt = lower_bound_adj(adj, first, e1, hi_t) - first;
+    const uint64_t key = stream_key(seed, side, 0, (uint64_t)v);
+    int32_t *row = out + (v - lo_s) * B;
+    for (int t = 0; t < B; ++t)
+      row[t] = cnt > 0 ? adj[first + draw_below(key, (uint64_t)t, cnt)] : -1;
+  }
+}
+}  // namespace
+}  // namespace tk
+}  // namespace gb
+
+GB_API int gb_fill_pool_side(const int64_t *xadj, const int32_t *adj, int64_t lo_s, int64_t hi_s,
+                             int64_t lo_t, int64_t hi_t, int B, uint64_t seed, uint64_t side,
+                             int32_t *out, void *stream_handle) {
+  GB_REQUIRE(xadj && out && B >= 1 && hi_s >= lo_s && hi_t >= lo_t,
+             "gb_fill_pool_side: bad args");
+  const int64_t n = hi_s - lo_s;
+  if (n == 0) return GB_OK;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+  gb::tk::fill_pool_kernel<<<(int)blocks, 256, 0, as_stream(stream_handle)>>>(
+      xadj, adj, lo_s, hi_s, lo_t, hi_t, B, seed, side, out);
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}

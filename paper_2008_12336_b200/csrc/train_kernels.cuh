@@ -418,15 +418,67 @@ __global__ void __launch_bounds__(kBlock) train_pool_kernel(PoolArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Fixed sample lists: source src[i] is updated against samples[i*k + j]
+// (j ascending, -1 = skip) with label labels[j]; single-array semantics of
+// update_embedding (trainer.py:137-142).  One group chains one source.
+// ---------------------------------------------------------------------------
+struct ListArgs {
+  float *M;
+  int dim;
+  int64_t n_src;
+  const int64_t *__restrict__ src;
+  int k;
+  const int64_t *__restrict__ samples;
+  const int8_t *__restrict__ labels;
+  double lr;
+  bool reuse;
+  int64_t max_groups;
+  int64_t *status;
+};
+
+template <class Row, bool EXACT>
+__global__ void __launch_bounds__(kBlock) apply_lists_kernel(ListArgs a) {
+  const GroupCtx g = group_ctx<Row>();
+  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / Row::G;
+  const int64_t ngroups =
+      min((int64_t)gridDim.x * blockDim.x / Row::G, a.max_groups > 0 ? a.max_groups : INT64_MAX);
+  if (gid >= ngroups) return;
+  bool bad = false;
+  for (int64_t i = gid; i < a.n_src; i += ngroups) {
+    const int64_t v = a.src[i];
+    Row S;
+    S.load(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+    for (int c0 = 0; c0 < a.k; c0 += kChunk) {
+      int64_t ids[kChunk];
+      double bs[kChunk];
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        const int idx = c0 + j;
+        ids[j] = idx < a.k ? a.samples[i * a.k + idx] : -1;
+        bs[j] = idx < a.k ? (double)a.labels[idx] : 0.0;
+      }
+      run_chunk<Row, EXACT>(S, v, ids, bs, a.M, a.dim, a.lr, a.reuse, true, false, g, bad);
+    }
+    S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+  }
+  if (bad && g.gl == 0) {
+    atomicOr(reinterpret_cast<unsigned long long *>(a.status), 1ull);
+    atomicMin(reinterpret_cast<long long *>(a.status + 1), 0ll);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Per-layout kernel table.
 // ---------------------------------------------------------------------------
 using PassFn = void (*)(PassArgs);
 using PoolFn = void (*)(PoolArgs);
+using ListFn = void (*)(ListArgs);
 
 struct Variant {
   int G = 0;
   PassFn pass = nullptr;
   PoolFn pool = nullptr;
+  ListFn lists = nullptr;
 };
 
 template <class Row, bool EXACT>
@@ -435,6 +487,7 @@ Variant make_variant() {
   v.G = Row::G;
   v.pass = train_passes_kernel<Row, EXACT>;
   v.pool = train_pool_kernel<Row, EXACT>;
+  v.lists = apply_lists_kernel<Row, EXACT>;
   return v;
 }
 

@@ -1,0 +1,324 @@
+"""CSR graph container and graph I/O (reference: graph.py).
+
+`Graph` keeps the reference's fields and methods (graph.py:23-77) but can be
+backed by device tensors: graphs built on the GPU (from_edges, the R-MAT
+generator, every coarse level) stay in HBM and only materialize their numpy
+`xadj`/`adj` when host code asks for them; host graphs upload once and cache
+the device copy.  CSR construction runs on the GPU (gb_csr_build: 64-bit
+key radix sort + unique + per-row binary search), producing exactly the
+reference's rows (strictly ascending, no duplicates, self-loops dropped).
+
+Text/binary I/O and the train/test split are host-side, as in the reference
+(they feed the hot path; SURVEY.md 2.1 marks them out of scope for
+acceleration).  The split keeps numpy's PCG64 stream so it selects the same
+edges as the reference for the same seed.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from dataclasses import dataclass
+from typing import IO, Iterable
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import EdgeListParseError, EmptyGraphError, SplitError
+
+GRAPH_MAGIC = b"GSHG"
+GRAPH_VERSION = 1
+
+
+class Graph:
+    """Compressed-sparse-row adjacency; `num_edges` counts stored arcs (an
+    undirected edge is two arcs).  Rows are strictly ascending."""
+
+    def __init__(self, num_vertices: int, num_edges: int, xadj: np.ndarray | None = None,
+                 adj: np.ndarray | None = None, directed: bool = False,
+                 orig_ids: np.ndarray | None = None, *, xadj_dev: torch.Tensor | None = None,
+                 adj_dev: torch.Tensor | None = None):
+        if xadj is None and xadj_dev is None:
+            raise ValueError("Graph needs host or device CSR arrays")
+        self.num_vertices = int(num_vertices)
+        self.num_edges = int(num_edges)
+        self.directed = bool(directed)
+        self.orig_ids = orig_ids
+        self._xadj = None if xadj is None else np.asarray(xadj)
+        self._adj = None if adj is None else np.asarray(adj)
+        self._xadj_dev = xadj_dev
+        self._adj_dev = adj_dev
+
+    # -- host view (lazy download) ---------------------------------------------
+    @property
+    def xadj(self) -> np.ndarray:
+        if self._xadj is None:
+            self._xadj = self._xadj_dev.cpu().numpy()
+        return self._xadj
+
+    @xadj.setter
+    def xadj(self, value) -> None:
+        self._xadj = np.asarray(value)
+        self._xadj_dev = None
+
+    @property
+    def adj(self) -> np.ndarray:
+        if self._adj is None:
+            if self._adj_dev is None:
+                self._adj = np.empty(0, dtype=np.int32)
+            else:
+                self._adj = self._adj_dev[: self.num_edges].cpu().numpy()
+        return self._adj
+
+    @adj.setter
+    def adj(self, value) -> None:
+        self._adj = np.asarray(value)
+        self._adj_dev = None
+
+    # -- device view (lazy upload) -----------------------------------------------
+    def device_csr(self) -> tuple[torch.Tensor, torch.Tensor]:
+        """(xadj int64[V+1], adj int32[max(E,1)]) on the current CUDA device."""
+        _lib.require_cuda()
+        if self._xadj_dev is None:
+            self._xadj_dev = torch.from_numpy(
+                np.ascontiguousarray(self._xadj, dtype=np.int64)).cuda()
+        if self._adj_dev is None:
+            a = np.ascontiguousarray(self.adj, dtype=np.int32)
+            if a.size == 0:
+                a = np.zeros(1, dtype=np.int32)
+            self._adj_dev = torch.from_numpy(a).cuda()
+        return self._xadj_dev, self._adj_dev
+
+    def drop_host(self) -> None:
+        """Forget the host copies of a device-resident graph."""
+        if self._xadj_dev is not None:
+            self._xadj = None
+            self._adj = None
+
+    @property
+    def on_device(self) -> bool:
+        return self._xadj_dev is not None
+
+    # -- reference methods (graph.py:37-77) --------------------------------------
+    def degree(self, v: int) -> int:
+        return int(self.xadj[v + 1] - self.xadj[v])
+
+    def neighbors(self, v: int) -> np.ndarray:
+        return self.adj[self.xadj[v]:self.xadj[v + 1]]
+
+    def has_arc(self, u: int, v: int) -> bool:
+        row = self.neighbors(u)
+        i = int(np.searchsorted(row, v))
+        return i < row.shape[0] and int(row[i]) == v
+
+    def degrees(self) -> np.ndarray:
+        return np.diff(self.xadj).astype(np.int64)
+
+    def undirected_pairs(self) -> np.ndarray:
+        """Arcs (u, v) with u < v as an (m, 2) array; each undirected edge once."""
+        src = np.repeat(np.arange(self.num_vertices, dtype=np.int64), np.diff(self.xadj))
+        dst = self.adj.astype(np.int64)
+        m = src < dst
+        return np.stack([src[m], dst[m]], axis=1)
+
+    def validate(self) -> None:
+        x, a = self.xadj, self.adj
+        if x.shape[0] != self.num_vertices + 1:
+            raise ValueError("xadj length must be |V|+1")
+        if x[0] != 0 or x[-1] != self.num_edges:
+            raise ValueError("xadj endpoints inconsistent with |E|")
+        steps = np.diff(x)
+        if (steps < 0).any():
+            raise ValueError("xadj must be nondecreasing")
+        if self.num_edges:
+            if a.min() < 0 or a.max() >= self.num_vertices:
+                raise ValueError("adj entry out of range")
+            # strictly ascending inside each row: a rise must occur at every
+            # position that is not a row start
+            row_start = np.zeros(self.num_edges, dtype=bool)
+            row_start[x[:-1][steps > 0]] = True
+            if (np.diff(a.astype(np.int64)) <= 0)[~row_start[1:]].any():
+                raise ValueError("adjacency rows must be strictly ascending")
+
+    def __repr__(self) -> str:
+        where = "device" if self.on_device else "host"
+        return (f"Graph(num_vertices={self.num_vertices}, num_edges={self.num_edges}, "
+                f"directed={self.directed}, {where})")
+
+
+@dataclass
+class SplitResult:
+    """Train graph plus withheld test edges (train-graph ids); kept_vertices
+    maps train id -> id in the split graph (graph.py:80-90)."""
+
+    train_graph: Graph
+    test_edges: np.ndarray
+    kept_vertices: np.ndarray
+
+
+def _csr_device(num_vertices: int, src: torch.Tensor, dst: torch.Tensor, flags: int,
+                directed: bool, orig_ids=None) -> Graph:
+    """gb_csr_build on device arc arrays (graph.py:93-109 semantics)."""
+    _lib.require_cuda()
+    src = src.to(device="cuda", dtype=torch.int64).contiguous()
+    dst = dst.to(device="cuda", dtype=torch.int64).contiguous()
+    n = int(src.numel())
+    cap = n * (2 if flags & _lib.GB_CSR_SYMMETRIZE else 1)
+    ws, wsb = _lib.workspace("gb_csr_build_workspace", num_vertices, n, flags)
+    xadj = torch.empty(num_vertices + 1, dtype=torch.int64, device="cuda")
+    adj = torch.empty(max(cap, 1), dtype=torch.int32, device="cuda")
+    ne = C.c_int64(0)
+    _lib.call("gb_csr_build", num_vertices, _lib.ptr(src) if n else None,
+              _lib.ptr(dst) if n else None, n, flags, _lib.ptr(xadj), _lib.ptr(adj),
+              C.byref(ne), _lib.ptr(ws), wsb, _lib.stream())
+    del ws
+    E = int(ne.value)
+    adj = adj[:max(E, 1)].clone() if cap > 2 * max(E, 1) else adj
+    return Graph(num_vertices, E, directed=directed, orig_ids=orig_ids, xadj_dev=xadj,
+                 adj_dev=adj)
+
+
+def from_edges(pairs: Iterable[tuple[int, int]] | np.ndarray, num_vertices: int | None = None,
+               directed: bool = False) -> Graph:
+    """CSR from (u, v) pairs over dense ids: self-loops and duplicate arcs
+    dropped, symmetrized unless directed (graph.py:112-131); built on the GPU."""
+    arr = np.asarray(pairs if isinstance(pairs, np.ndarray) else list(pairs), dtype=np.int64)
+    arr = arr.reshape(-1, 2)
+    if num_vertices is None:
+        num_vertices = int(arr.max()) + 1 if arr.size else 0
+    if num_vertices == 0:
+        raise EmptyGraphError("graph has no vertices")
+    flags = _lib.GB_CSR_DROP_SELF | (0 if directed else _lib.GB_CSR_SYMMETRIZE)
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    return _csr_device(int(num_vertices), t[:, 0], t[:, 1], flags, directed)
+
+
+def densify(g: Graph) -> tuple[Graph, np.ndarray]:
+    """Drop isolated vertices and re-number the rest in ascending order (the
+    load_edge_list convention, graph.py:160-164), on the GPU.  Returns the new
+    graph and kept (new id -> old id)."""
+    xadj, adj = g.device_csr()
+    V, E = g.num_vertices, g.num_edges
+    ws, wsb = _lib.workspace("gb_csr_densify_workspace", V)
+    x2 = torch.empty(V + 1, dtype=torch.int64, device="cuda")
+    a2 = torch.empty(max(E, 1), dtype=torch.int32, device="cuda")
+    new_id = torch.empty(V, dtype=torch.int64, device="cuda")
+    kept = torch.empty(V, dtype=torch.int64, device="cuda")
+    nk = C.c_int64(0)
+    _lib.call("gb_csr_densify", V, E, _lib.ptr(xadj), _lib.ptr(adj), _lib.ptr(x2), _lib.ptr(a2),
+              _lib.ptr(new_id), _lib.ptr(kept), C.byref(nk), _lib.ptr(ws), wsb, _lib.stream())
+    k = int(nk.value)
+    if k == 0:
+        raise EmptyGraphError("graph has no non-isolated vertex")
+    kept_h = kept[:k].cpu().numpy()
+    return Graph(k, E, directed=g.directed, xadj_dev=x2[:k + 1].clone(), adj_dev=a2), kept_h
+
+
+def load_edge_list(text_stream: IO[str], directed: bool = False) -> Graph:
+    """Edge-list text, one "u v" per line, '#' comments and blank lines
+    skipped; ids densified in ascending order with the originals kept in
+    orig_ids (graph.py:134-171).  Parsing is host work; the CSR is built on
+    the GPU."""
+    us: list[int] = []
+    vs: list[int] = []
+    for lineno, raw in enumerate(text_stream, start=1):
+        line = raw.strip()
+        if not line or line[0] == "#":
+            continue
+        fields = line.split()
+        if len(fields) != 2:
+            raise EdgeListParseError(lineno, f"expected two fields, got {len(fields)}")
+        try:
+            u, v = int(fields[0]), int(fields[1])
+        except ValueError:
+            raise EdgeListParseError(lineno, f"non-integer vertex id in {line!r}") from None
+        us.append(u)
+        vs.append(v)
+    if not us:
+        raise EmptyGraphError("edge list contains no edges")
+    u_arr = np.asarray(us, dtype=np.int64)
+    v_arr = np.asarray(vs, dtype=np.int64)
+    ids = np.unique(np.concatenate([u_arr, v_arr]))
+    src = torch.from_numpy(np.searchsorted(ids, u_arr).astype(np.int64))
+    dst = torch.from_numpy(np.searchsorted(ids, v_arr).astype(np.int64))
+    flags = _lib.GB_CSR_DROP_SELF | (0 if directed else _lib.GB_CSR_SYMMETRIZE)
+    return _csr_device(int(ids.shape[0]), src, dst, flags, directed, orig_ids=ids)
+
+
+def write_edge_list(g: Graph, text_stream: IO[str]) -> None:
+    """Inverse of load_edge_list up to densification (graph.py:174-185)."""
+    if g.directed:
+        src = np.repeat(np.arange(g.num_vertices, dtype=np.int64), np.diff(g.xadj))
+        pairs = np.stack([src, g.adj.astype(np.int64)], axis=1)
+    else:
+        pairs = g.undirected_pairs()
+    names = g.orig_ids if g.orig_ids is not None else np.arange(g.num_vertices)
+    text_stream.writelines(f"{names[a]} {names[b]}\n" for a, b in pairs)
+
+
+def degree(g: Graph, v: int) -> int:
+    """Number of arcs leaving v."""
+    return g.degree(v)
+
+
+def save_graph(g: Graph, path: str) -> None:
+    """GSHG binary cache: magic, u32 version, u64 V, u64 E, u64 xadj[V+1],
+    u32 adj[E], little-endian (graph.py:192-200)."""
+    header = GRAPH_MAGIC + struct.pack("<IQQ", GRAPH_VERSION, g.num_vertices, g.num_edges)
+    with open(path, "wb") as f:
+        f.write(header)
+        f.write(np.ascontiguousarray(g.xadj, dtype="<u8").tobytes())
+        f.write(np.ascontiguousarray(g.adj, dtype="<u4").tobytes())
+
+
+def load_graph(path: str, directed: bool = False) -> Graph:
+    """Read a GSHG file written by save_graph (graph.py:203-219)."""
+    with open(path, "rb") as f:
+        magic = f.read(4)
+        if magic != GRAPH_MAGIC:
+            raise ValueError(f"bad magic {magic!r}, expected {GRAPH_MAGIC!r}")
+        (version,) = struct.unpack("<I", f.read(4))
+        if version != GRAPH_VERSION:
+            raise ValueError(f"unsupported cache version {version}")
+        nv, ne = struct.unpack("<QQ", f.read(16))
+        xadj = np.fromfile(f, dtype="<u8", count=nv + 1).astype(np.int64)
+        adj = np.fromfile(f, dtype="<u4", count=ne).astype(np.int32)
+    g = Graph(int(nv), int(ne), xadj=xadj, adj=adj, directed=directed)
+    g.validate()
+    return g
+
+
+def split_train_test(g: Graph, test_fraction: float, seed: int) -> SplitResult:
+    """Withhold round(fraction * m) undirected edges chosen by numpy PCG64
+    (same draw as graph.py:242-244), drop vertices left isolated and
+    re-densify; test edges losing an endpoint are dropped (graph.py:222-265).
+    The train CSR is built on the GPU."""
+    if g.directed:
+        raise SplitError("split requires an undirected graph")
+    if not 0.0 < test_fraction < 1.0:
+        raise SplitError(f"test_fraction must be in (0, 1), got {test_fraction}")
+    pairs = g.undirected_pairs()
+    m = pairs.shape[0]
+    k = int(round(test_fraction * m))
+    if k < 1:
+        raise SplitError(f"graph too small to withhold any edge "
+                         f"({m} edges at fraction {test_fraction})")
+    if k >= m:
+        raise SplitError("withholding would leave no training edges")
+    chosen = np.random.default_rng(seed).choice(m, size=k, replace=False)
+    is_test = np.zeros(m, dtype=bool)
+    is_test[chosen] = True
+    train, test = pairs[~is_test], pairs[is_test]
+    used = np.zeros(g.num_vertices, dtype=bool)
+    used[train.ravel()] = True
+    kept = np.flatnonzero(used)
+    relabel = np.full(g.num_vertices, -1, dtype=np.int64)
+    relabel[kept] = np.arange(kept.shape[0])
+    tr = relabel[train]
+    orig = g.orig_ids[kept] if g.orig_ids is not None else kept.copy()
+    tg = _csr_device(int(kept.shape[0]), torch.from_numpy(np.ascontiguousarray(tr[:, 0])),
+                     torch.from_numpy(np.ascontiguousarray(tr[:, 1])),
+                     _lib.GB_CSR_DROP_SELF | _lib.GB_CSR_SYMMETRIZE, False, orig_ids=orig)
+    te = relabel[test]
+    te = te[(te >= 0).all(axis=1)]
+    return SplitResult(train_graph=tg, test_edges=te, kept_vertices=kept)

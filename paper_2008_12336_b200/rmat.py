@@ -1,0 +1,62 @@
+"""Synthetic R-MAT input on the GPU (the reference has no
+generator).
+
+Graph500 parameters (a, b, c, d) = (0.57, 0.19, 0.19, 0.05); every edge is a
+pure function of (seed, edge index) through the reference's splitmix64
+streams (key(seed, 'RMAT', e, 0), one draw per level), ids are relabelled by
+a seeded permutation (stable sort of draw_u64(key(seed, 'PERM', 0, 0), i)),
+then the arcs go through the same CSR build as from_edges (self-loops and
+duplicates dropped, symmetrized).  Multilevel configs densify ids the way
+load_edge_list does.  oracle/gosh_oracle.c restates the generator on the CPU
+for the parity tests; the fixture tests pin it against the reference's
+from_edges.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .graph import Graph, _csr_device, densify
+
+RMAT_ABCD = (0.57, 0.19, 0.19, 0.05)
+
+
+def rmat_edges(scale: int, num_samples: int, seed: int, permute: bool = True,
+               abc=RMAT_ABCD[:3]) -> tuple[torch.Tensor, torch.Tensor]:
+    """Raw sampled (src, dst) int64 device arrays over 2^scale ids."""
+    _lib.require_cuda()
+    a, b, c = abc
+    st = _lib.stream()
+    perm = None
+    if permute:
+        ws, wsb = _lib.workspace("gb_rmat_permutation_workspace", scale)
+        perm = torch.empty(1 << scale, dtype=torch.int64, device="cuda")
+        _lib.call("gb_rmat_permutation", scale, _lib.u64(seed), _lib.ptr(perm), _lib.ptr(ws),
+                  wsb, st)
+        del ws
+    src = torch.empty(num_samples, dtype=torch.int64, device="cuda")
+    dst = torch.empty(num_samples, dtype=torch.int64, device="cuda")
+    _lib.call("gb_rmat_edges", scale, num_samples, a, a + b, a + b + c, _lib.u64(seed),
+              _lib.ptr(perm), _lib.ptr(src), _lib.ptr(dst), st)
+    return src, dst
+
+
+def rmat_graph(scale: int, num_samples: int, seed: int = 7, densify_ids: bool = False,
+               permute: bool = True) -> Graph:
+    """Undirected R-MAT CSR on the device.  With densify_ids, isolated ids
+    are dropped (orig_ids holds the surviving raw ids)."""
+    src, dst = rmat_edges(scale, num_samples, seed, permute)
+    g = _csr_device(1 << scale, src, dst, _lib.GB_CSR_DROP_SELF | _lib.GB_CSR_SYMMETRIZE, False)
+    del src, dst
+    if densify_ids:
+        g2, kept = densify(g)
+        g2.orig_ids = kept
+        return g2
+    return g
+
+
+def samples_for_edges(target_undirected_edges: int, keep_ratio: float = 0.81) -> int:
+    """Oversampling to reach a target count of unique undirected edges
+    (dedup keeps ~81% at scale 14 and ~94% at scale 20)."""
+    return int(np.ceil(target_undirected_edges / keep_ratio))

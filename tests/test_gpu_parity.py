@@ -1,0 +1,368 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the reference's
+golden vectors and the CPU oracle.
+
+Bars (north star): bit-exact for RNG, CSR, coarsening maps and levels, pools
+and every deterministic training result; within 1e-5 relative for the
+parallel (tree-dot / Hogwild) kernels on fixed sample lists.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2008_12336_b200 as gb
+from paper_2008_12336_b200 import _lib
+from paper_2008_12336_b200.graph import Graph
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-5
+
+
+def _graphs(g, prefix="g"):
+    out = []
+    i = 0
+    while f"{prefix}{i}_xadj" in g:
+        x, a = g[f"{prefix}{i}_xadj"], g[f"{prefix}{i}_adj"]
+        out.append(Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a))
+        i += 1
+    return out
+
+
+def _rel_err(a, b):
+    return float(np.max(np.abs(a.astype(np.float64) - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+# -- RNG --------------------------------------------------------------------------
+def test_device_rng_matches_reference(cuda, golden):
+    t = golden("rng.npz")["table"]
+    for row in t[::7].tolist():
+        seed, stream, step, v, ctr, n, key, d = row
+        out = torch.empty(3, dtype=torch.int64, device=cuda)
+        _lib.call("gb_rng_draw_below", seed, stream, step, v, ctr, n, 3, _lib.ptr(out),
+                  _lib.stream())
+        assert int(out[0]) == d
+
+
+def test_device_rng_batch_matches_oracle(cuda, orc):
+    out = torch.empty(100000, dtype=torch.int64, device=cuda)
+    _lib.call("gb_rng_draw_below", 5, 3, 9, 1000, 2, 123457, 100000, _lib.ptr(out),
+              _lib.stream())
+    assert np.array_equal(out.cpu().numpy(), orc.rng_draw_below(5, 3, 9, 1000, 2, 123457, 100000))
+
+
+# -- CSR build / R-MAT --------------------------------------------------------------
+def test_from_edges_matches_reference(cuda, golden):
+    g = golden("csr.npz")
+    for k in range(int(g["n"])):
+        pairs = g[f"c{k}_pairs"]
+        h = gb.from_edges(pairs, num_vertices=int(g[f"c{k}_V"]),
+                          directed=bool(g[f"c{k}_directed"]))
+        assert np.array_equal(h.xadj, g[f"c{k}_xadj"]), k
+        assert np.array_equal(h.adj, g[f"c{k}_adj"]), k
+        h.validate()
+
+
+def test_from_edges_small_cases(cuda):
+    g = gb.from_edges([(0, 1), (1, 0), (1, 2), (2, 2)], num_vertices=3)
+    assert g.num_edges == 4 and g.xadj.tolist() == [0, 1, 3, 4] and g.adj.tolist() == [1, 0, 2, 1]
+    d = gb.from_edges([(0, 1), (2, 1)], num_vertices=3, directed=True)
+    assert d.has_arc(0, 1) and not d.has_arc(1, 0)
+    e = gb.from_edges(np.zeros((0, 2), np.int64), num_vertices=4)
+    assert e.num_edges == 0 and e.xadj.tolist() == [0] * 5
+    with pytest.raises(gb.EmptyGraphError):
+        gb.from_edges([], num_vertices=0)
+
+
+def test_rmat_generator_matches_oracle_and_reference(cuda, orc, golden):
+    g = golden("rmat.npz")
+    for k in range(2):
+        scale, n, seed = g[f"r{k}_cfg"].tolist()
+        src, dst = gb.rmat_edges(scale, n, seed)
+        assert np.array_equal(src.cpu().numpy(), g[f"r{k}_src"])
+        assert np.array_equal(dst.cpu().numpy(), g[f"r{k}_dst"])
+        h = gb.rmat_graph(scale, n, seed)
+        assert np.array_equal(h.xadj, g[f"r{k}_xadj"]) and np.array_equal(h.adj, g[f"r{k}_adj"])
+    # a larger instance against the oracle, raw and densified
+    x, a = orc.rmat_graph(14, 1 << 18, 11)
+    h = gb.rmat_graph(14, 1 << 18, 11)
+    assert np.array_equal(h.xadj, x) and np.array_equal(h.adj, a)
+    xd, ad = orc.rmat_graph(14, 1 << 18, 11, densify_ids=True)
+    hd = gb.rmat_graph(14, 1 << 18, 11, densify_ids=True)
+    assert np.array_equal(hd.xadj, xd) and np.array_equal(hd.adj, ad)
+    hd.validate()
+
+
+def test_load_edge_list_and_split(cuda, tmp_path):
+    import io
+    g = gb.load_edge_list(io.StringIO("# c\n5 9\n9 40\n\n40 5\n"))
+    assert g.num_vertices == 3 and g.orig_ids.tolist() == [5, 9, 40] and g.num_edges == 6
+    g = gb.rmat_graph(10, 4000, 3, densify_ids=True)
+    a = gb.split_train_test(g, 0.2, seed=4)
+    b = gb.split_train_test(g, 0.2, seed=4)
+    assert np.array_equal(a.test_edges, b.test_edges)
+    tg = a.train_graph
+    tg.validate()
+    assert np.all(tg.degrees() > 0)
+    for u, v in a.test_edges[:50]:
+        assert not tg.has_arc(int(u), int(v))
+
+
+# -- coarsening -------------------------------------------------------------------------
+def test_coarsening_matches_reference_goldens(cuda, golden):
+    g = golden("coarsen.npz")
+    for i, name in enumerate(g["names"].tolist()):
+        x, a = g[f"g{i}_xadj"], g[f"g{i}_adj"]
+        G = Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
+        order = gb.degree_order(G)
+        assert np.array_equal(order, g[f"g{i}_order"]), name
+        m = gb.collapse_map(G, order)
+        assert m.num_clusters == int(g[f"g{i}_nc"]), name
+        assert np.array_equal(m.map, g[f"g{i}_map"]), name
+        cg = gb.build_coarse_graph(G, m)
+        assert np.array_equal(cg.xadj, g[f"g{i}_cxadj"]), name
+        assert np.array_equal(cg.adj, g[f"g{i}_cadj"]), name
+        h = gb.coarsen_all(G, threshold=int(g[f"g{i}_thr"]))
+        assert h.depth == int(g[f"g{i}_depth"]) and h.stalled == bool(g[f"g{i}_stalled"]), name
+        for L in range(1, h.depth):
+            assert np.array_equal(h.graphs[L].xadj, g[f"g{i}_L{L}_xadj"]), (name, L)
+            assert np.array_equal(h.graphs[L].adj, g[f"g{i}_L{L}_adj"]), (name, L)
+            assert np.array_equal(h.mappings[L - 1].map, g[f"g{i}_M{L - 1}_map"]), (name, L)
+
+
+@pytest.mark.parametrize("scale,samples,dens", [(16, 1 << 20, True), (17, 1 << 21, False)])
+def test_coarsen_all_bit_exact_on_rmat(cuda, orc, scale, samples, dens):
+    x, a = orc.rmat_graph(scale, samples, 7, densify_ids=dens)
+    graphs, maps, stalled = orc.coarsen_all(x, a, 100)
+    G = gb.rmat_graph(scale, samples, 7, densify_ids=dens)
+    h = gb.coarsen_all(G, threshold=100)
+    assert h.depth == len(graphs) and h.stalled == stalled
+    for L in range(1, h.depth):
+        assert np.array_equal(h.graphs[L].xadj, graphs[L][0])
+        assert np.array_equal(h.graphs[L].adj, graphs[L][1])
+        assert np.array_equal(h.mappings[L - 1].map, maps[L - 1][0])
+
+
+def test_directed_collapse_matches_oracle(cuda, orc):
+    rng = np.random.default_rng(2)
+    pairs = rng.integers(0, 300, size=(1500, 2))
+    G = gb.from_edges(pairs, num_vertices=300, directed=True)
+    order = gb.degree_order(G)
+    cmap, nc = orc.collapse_seq(G.xadj, G.adj, order)
+    m = gb.collapse_map(G, order)
+    assert m.num_clusters == nc and np.array_equal(m.map, cmap)
+
+
+def test_expand_matches_oracle(cuda, orc):
+    rng = np.random.default_rng(1)
+    for d in (3, 8, 32, 128):
+        coarse = rng.random((40, d)).astype(np.float32)
+        cmap = rng.integers(0, 40, size=1000).astype(np.int32)
+        got = gb.expand_embedding(coarse, gb.Mapping(map=cmap, num_clusters=40))
+        assert np.array_equal(got, orc.expand(coarse, cmap))
+    with pytest.raises(ValueError):
+        gb.expand_embedding(coarse[:3], gb.Mapping(map=cmap, num_clusters=40))
+
+
+# -- training: exact (deterministic) kernels vs the reference ---------------------------
+def test_update_embedding_bit_exact(cuda, golden):
+    g = golden("update.npz")
+    for k, (d, b, reuse, v, s, lr) in enumerate(g["cases"].tolist()):
+        M = g[f"c{k}_before"].copy()
+        gb.update_embedding(M, int(v), int(s), int(b), lr, reuse_updated_source=bool(reuse))
+        assert np.array_equal(M, g[f"c{k}_after"]), k
+    with pytest.raises(TypeError):
+        gb.update_embedding(np.zeros((2, 4)), 0, 1, 1, 0.1)
+
+
+def test_train_pass_exact_bit_exact_vs_reference(cuda, golden):
+    g = golden("train_pass.npz")
+    graphs = _graphs(g)
+    for k, (gi, d, n_neg, reuse, seed, stream, lr) in enumerate(g["cases"].tolist()):
+        G = graphs[int(gi)]
+        M = torch.from_numpy(g[f"c{k}_M0"].copy()).cuda()
+        lrs = torch.full((3,), lr, dtype=torch.float32, device="cuda")
+        st = _lib.new_status()
+        x, a = G.device_csr()
+        flags = _lib.GB_TRAIN_EXACT | (_lib.GB_TRAIN_REUSE if reuse else 0)
+        _lib.call("gb_train_passes", G.num_vertices, _lib.ptr(x), _lib.ptr(a), _lib.ptr(M),
+                  int(d), int(n_neg), int(seed), int(stream), 0, 3, 1, _lib.ptr(lrs), flags, 1,
+                  _lib.ptr(st), _lib.stream())
+        assert np.array_equal(M.cpu().numpy(), g[f"c{k}_M3"]), k
+
+
+def test_train_level_deterministic_bit_exact(cuda, golden):
+    g = golden("train_pass.npz")
+    graphs = _graphs(g)
+    for j, (gi, d, e_i, seed, stream, edge, passes, updates) in enumerate(g["levels"].tolist()):
+        cfg = gb.TrainConfig(dim=d, total_epochs=e_i, seed=seed, negative_samples=3,
+                             learning_rate=0.05, deterministic=True,
+                             epoch_unit="edge-scaled" if edge else "vertex-pass")
+        M = g[f"L{j}_M0"].copy()
+        st = gb.train_level(graphs[gi], M, cfg, e_i, rng_stream=stream)
+        assert st == (passes, updates)
+        assert np.array_equal(M, g[f"L{j}_M"]), j
+
+
+def test_train_multilevel_deterministic_bit_exact(cuda, golden):
+    g = golden("large.npz")
+    for k, (d, e, p10, edge, seed, thr, depth) in enumerate(g["multilevel"].tolist()):
+        x, a = g[f"ml{k}_0_xadj"], g[f"ml{k}_0_adj"]
+        G = Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
+        cfg = gb.TrainConfig(dim=d, total_epochs=e, smoothing_ratio=p10 / 10, seed=seed,
+                             epoch_unit="edge-scaled" if edge else "vertex-pass",
+                             deterministic=True)
+        h = gb.coarsen_all(G, threshold=thr)
+        assert h.depth == depth
+        M = gb.train_multilevel(G, cfg, hierarchy=h)
+        assert np.array_equal(M, g[f"ml{k}_M"]), k
+
+
+# -- training: parallel kernels within 1e-5 on fixed sample lists -----------------------
+@pytest.mark.parametrize("d", [8, 32, 33, 128, 256])
+def test_tree_dot_single_group_within_tolerance(cuda, orc, d):
+    """Fast layout (tree dot) with one group in flight = the reference's update
+    order; only the fp64 summation order differs."""
+    x, a = orc.rmat_graph(11, 16000, 5, densify_ids=True)
+    G = Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
+    M0 = orc.init_embedding(G.num_vertices, d, 3)
+    M = M0.copy()
+    cfg = gb.TrainConfig(dim=d, seed=3, max_inflight=1)
+    gb.train_level(G, M, cfg, 2, lr0=0.035, rng_stream=1)
+    # lr decays per epoch in train_level; replay that schedule in the oracle
+    ref = M0.copy()
+    orc.train_level(x, a, ref, d, 2, 0.035, 3, 3, 1)
+    assert _rel_err(M, ref) <= REL_TOL
+
+
+def test_fixed_sample_lists_parallel_within_tolerance(cuda, orc):
+    """One deterministic update epoch on fixed sample lists: disjoint sources
+    and sample rows run fully parallel and must match the sequential oracle."""
+    rng = np.random.default_rng(8)
+    V, d, n = 40000, 128, 4000
+    M0 = orc.init_embedding(V, d, 1) * 40.0  # larger rows: non-trivial scores
+    perm = rng.permutation(V)
+    src = perm[:n]
+    samples = perm[n:n + 4 * n].reshape(n, 4)
+    labels = np.array([1, 0, 0, 0], dtype=np.int8)
+    M = M0.copy()
+    gb.apply_sample_lists(M, src, samples, labels, 0.05)
+    ref = M0.copy()
+    for i in range(n):
+        for j in range(4):
+            orc.update_embedding(ref, int(src[i]), int(samples[i, j]), int(labels[j]), 0.05)
+    assert _rel_err(M, ref) <= REL_TOL
+    M2 = M0.copy()
+    gb.apply_sample_lists(M2, src, samples, labels, 0.05, deterministic=True)
+    assert np.array_equal(M2, ref)
+
+
+def test_hogwild_pass_counts_and_finiteness(cuda, orc):
+    G = gb.rmat_graph(16, 1 << 20, 2)
+    M = torch.from_numpy(orc.init_embedding(G.num_vertices, 128, 1)).cuda()
+    before = M.clone()
+    cfg = gb.TrainConfig(dim=128, seed=1)
+    st = gb.train_level(G, M, cfg, 3)
+    non_iso = int((G.degrees() > 0).sum())
+    assert st.passes == 3 and st.updates == 3 * non_iso * 4
+    assert torch.isfinite(M).all()
+    moved = (M != before).any(dim=1).cpu().numpy()
+    assert moved[G.degrees() > 0].all()
+
+
+def test_nonfinite_is_reported(cuda):
+    G = gb.from_edges([(0, 1), (1, 2), (2, 3)], num_vertices=5)
+    M = np.full((5, 8), 0.01, np.float32)
+    M[4, 3] = np.nan  # untouched isolated row: caught by the full scan
+    with pytest.raises(FloatingPointError):
+        gb.train_level(G, M, gb.TrainConfig(dim=8), 1)
+    M = np.full((5, 8), 0.01, np.float32)
+    M[1, 0] = np.inf
+    with pytest.raises(FloatingPointError):
+        gb.train_level(G, M, gb.TrainConfig(dim=8), 1)
+
+
+def test_train_level_edge_cases(cuda):
+    G = gb.from_edges([(0, 1)], num_vertices=1 + 1)
+    M = gb.init_embedding(2, 4, 1)
+    before = M.copy()
+    assert gb.train_level(G, M, gb.TrainConfig(dim=4), 0) == (0, 0)
+    assert np.array_equal(M, before)
+    with pytest.raises(ValueError):
+        gb.train_level(G, M[:1], gb.TrainConfig(dim=4), 1)
+    K6 = gb.from_edges([(i, j) for i in range(6) for j in range(i + 1, 6)], num_vertices=6)
+    st = gb.train_level(K6, gb.init_embedding(6, 8, 1),
+                        gb.TrainConfig(dim=8, epoch_unit="edge-scaled"), 2)
+    assert st.passes == 10
+    M0 = gb.train_multilevel(K6, gb.TrainConfig(dim=8, total_epochs=0, seed=3), no_coarsen=True)
+    assert np.array_equal(M0, gb.init_embedding(6, 8, 3))
+
+
+# -- partitioned path ---------------------------------------------------------------------
+def test_pools_and_train_pair_bit_exact(cuda, golden):
+    g = golden("pool.npz")
+    graphs = _graphs(g)
+    for k, row in enumerate(g["cases"].tolist()):
+        gi, j, kk, lo_j, hi_j, lo_k, hi_k, d, B, n_neg, reuse, seed, lr, pos = row
+        gi, j, kk, B, n_neg, seed, pos = map(int, (gi, j, kk, B, n_neg, seed, pos))
+        G = graphs[gi]
+        n = G.num_vertices
+        plan = gb.PartitionPlan(K=3, boundaries=(np.arange(4, dtype=np.int64) * n) // 3)
+        pool = gb.build_sample_pool(G, plan, (j, kk), B, seed)
+        assert np.array_equal(pool.targets_j, g[f"c{k}_tj"]), k
+        if j != kk:
+            assert np.array_equal(pool.targets_k, g[f"c{k}_tk"]), k
+        Mj = g[f"c{k}_Mj0"].copy()
+        Mk = Mj if j == kk else g[f"c{k}_Mk0"].copy()
+        got = gb.train_pair(Mj, Mk, pool, n_neg, lr, seed, reuse_updated_source=bool(reuse),
+                            deterministic=True)
+        assert got == pos
+        assert np.array_equal(Mj, g[f"c{k}_Mj"]), (k, "j")
+        assert np.array_equal(Mk, g[f"c{k}_Mk"]), (k, "k")
+
+
+def test_fused_pool_equals_materialized(cuda, orc):
+    x, a = orc.rmat_graph(12, 40000, 9, densify_ids=True)
+    G = Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
+    n = G.num_vertices
+    lo_j, hi_j, lo_k, hi_k = 0, n // 3, n // 3, 2 * n // 3
+    M0 = orc.init_embedding(n, 32, 4)
+    B, n_neg, lr, seed = 5, 3, 0.05, 77
+    tj = orc.fill_pool_side(x, a, lo_j, hi_j, lo_k, hi_k, B, seed, 0)
+    ref = M0.copy()
+    Mj, Mk = ref[lo_j:hi_j].copy(), ref[lo_k:hi_k].copy()
+    want_pos = orc.train_pool_side(Mj, Mk, tj, lo_k, hi_k - lo_k, n_neg, lr, seed, 2)
+    dj = torch.from_numpy(M0[lo_j:hi_j].copy()).cuda()
+    dk = torch.from_numpy(M0[lo_k:hi_k].copy()).cuda()
+    st = _lib.new_status()
+    xa, aa = G.device_csr()
+    _lib.call("gb_train_pool_side", _lib.ptr(dj), _lib.ptr(dk), 32, None, hi_j - lo_j, B, lo_k,
+              hi_k - lo_k, n_neg, lr, seed, 2, _lib.ptr(xa), _lib.ptr(aa), lo_j, 0,
+              _lib.GB_TRAIN_EXACT, 1, _lib.ptr(st), _lib.stream())
+    assert np.array_equal(dj.cpu().numpy(), Mj) and np.array_equal(dk.cpu().numpy(), Mk)
+    assert int(st[2]) == want_pos
+
+
+def test_train_large_deterministic_bit_exact(cuda, golden):
+    g = golden("large.npz")
+    G = _graphs(g)[0]
+    for k, row in enumerate(g["large"].tolist()):
+        d, e_i, B, edge, reuse, seed, res, rot, K, sw, pos = row
+        cfg = gb.TrainConfig(dim=d, total_epochs=e_i, seed=seed, negative_samples=2,
+                             epoch_unit="edge-scaled" if edge else "vertex-pass",
+                             reuse_updated_source=bool(reuse), deterministic=True)
+        M = g[f"r{k}_M0"].copy()
+        st = gb.train_large(G, M, cfg, e_i, gb.MemoryBudget(res, batch_size=B), rng_stream=k)
+        assert (st["rotations"], st["K"], st["switches"], st["pos_updates"]) == (rot, K, sw, pos)
+        assert st["peak_bytes"] <= st["budget_bytes"]
+        assert np.array_equal(M, g[f"r{k}_M"]), k
+
+
+def test_train_large_device_matrix_hogwild(cuda, orc):
+    G = gb.rmat_graph(12, 40000, 1, densify_ids=True)
+    cfg = gb.TrainConfig(dim=32, seed=2, negative_samples=3)
+    M = torch.from_numpy(orc.init_embedding(G.num_vertices, 32, 2)).cuda()
+    budget = gb.MemoryBudget(3 * 32 * 4 * (G.num_vertices // 4 + 1) + 4 * 2 * 5 * 4 * G.num_vertices)
+    st = gb.train_large(G, M, cfg, 10, budget)
+    assert st["K"] >= 3 and st["pos_updates"] > 0 and torch.isfinite(M).all()
