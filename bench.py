@@ -206,7 +206,7 @@ def run_ours(args):
     build_s = time.perf_counter() - t_build
     xadj, adj = G.device_csr()
     V = G.num_vertices
-    non_iso = int((xadj[1:] > xadj[:-1]).sum().item())
+    sources, non_iso = G.active_sources()
     M = torch.from_numpy(gb.init_embedding(V, DIM, 1)).to(dev)
     lrs = torch.tensor([np.float32(LR)], dtype=torch.float32, device=dev)
     status = _lib.new_status()
@@ -214,7 +214,8 @@ def run_ours(args):
     cap = gb.trainer.inflight_cap(gb.TrainConfig(dim=DIM), V)
 
     def launch(p):
-        _lib.call("gb_train_passes", V, _lib.ptr(xadj), _lib.ptr(adj), _lib.ptr(M), DIM, NNEG,
+        _lib.call("gb_train_passes", V, _lib.ptr(xadj), _lib.ptr(adj), _lib.ptr(sources),
+                  non_iso, _lib.ptr(M), DIM, NNEG,
                   1, 0, p, 1, 1 << 40, _lib.ptr(lrs), 0, cap, _lib.ptr(status),
                   stream.cuda_stream)
 

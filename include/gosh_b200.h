@@ -85,6 +85,13 @@ int gb_csr_densify(int64_t num_vertices, int64_t num_edges,
                    int64_t *num_kept_out, void *workspace, size_t ws_bytes,
                    void *stream_handle);
 
+/* Non-isolated vertices in ascending id order (the sources a training pass
+ * visits, trainer.py:198-200).  Synchronizes; writes the count. */
+int gb_active_sources_workspace(int64_t num_vertices, size_t *bytes);
+int gb_active_sources(int64_t num_vertices, const int64_t *xadj, int32_t *out,
+                      int64_t *count_out, void *workspace, size_t ws_bytes,
+                      void *stream_handle);
+
 /* ---- synthetic input: Graph500 R-MAT edge sampler -------
  * Writes num_samples (src,dst) pairs over 2^scale ids; ids are relabelled by
  * the seeded permutation perm (perm[i] = i-th id of the stable argsort of
@@ -137,9 +144,12 @@ int gb_expand(const float *coarse, int64_t num_clusters, int dim,
  * owned by "groups" (G lanes of a warp); max_groups caps how many sources are
  * in flight at once (0 = fill the GPU).  GB_TRAIN_EXACT runs one group in
  * the reference's sequential order with the reference's serial fp64 dot and
- * reproduces _train_pass(num_workers=1) bit-for-bit.  status: see above. */
+ * reproduces _train_pass(num_workers=1) bit-for-bit.  sources (optional,
+ * from gb_active_sources) lists the non-isolated vertices in ascending order
+ * so lanes never idle on isolated ids; NULL scans all V.  status: above. */
 int gb_train_passes(int64_t num_vertices, const int64_t *xadj,
-                    const int32_t *adj, float *M, int dim, int n_neg,
+                    const int32_t *adj, const int32_t *sources,
+                    int64_t n_sources, float *M, int dim, int n_neg,
                     uint64_t seed, uint64_t rng_stream, int64_t pass_begin,
                     int64_t n_passes, int64_t passes_per_epoch,
                     const float *lr_per_epoch, unsigned flags,

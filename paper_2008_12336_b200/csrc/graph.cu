@@ -175,6 +175,14 @@ __global__ void remap_adj(const int32_t *__restrict__ adj, int64_t E,
   GRID_STRIDE(e, E) adj_out[e] = (int32_t)new_id[adj[e]];
 }
 
+__global__ void active_flags(const int64_t *__restrict__ xadj, int64_t V,
+                             int32_t *__restrict__ ids, char *__restrict__ flag) {
+  GRID_STRIDE(v, V) {
+    ids[v] = (int32_t)v;
+    flag[v] = xadj[v + 1] > xadj[v];
+  }
+}
+
 __global__ void set_tail(int64_t *__restrict__ xadj_out, const int64_t *__restrict__ count,
                          int64_t E) {
   xadj_out[*count] = E;
@@ -446,8 +454,8 @@ GB_API int gb_csr_build(int64_t num_vertices, const int64_t *src, const int64_t 
 GB_API int gb_csr_densify_workspace(int64_t num_vertices, size_t *bytes) {
   GB_REQUIRE(num_vertices >= 1 && bytes, "gb_csr_densify_workspace: bad args");
   Carver c(nullptr);
-  c.take<int64_t>(num_vertices);
-  c.take<int64_t>(num_vertices);
+  c.take<int64_t>(num_vertices + 1);
+  c.take<int64_t>(num_vertices + 1);
   c.take<int64_t>(1);
   size_t scan_bytes = 0;
   GB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int64_t *)nullptr,
@@ -741,5 +749,56 @@ GB_API int gb_expand(const float *coarse, int64_t num_clusters, int dim, const i
     expand_scalar<<<blocks_for(num_rows * dim), 256, 0, st>>>(coarse, cmap, num_rows, dim, out);
   }
   GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
+static int active_layout(Carver &c, int64_t V, int32_t **ids, char **flag, int64_t **cnt,
+                         void **tmp, size_t *tb) {
+  *ids = c.take<int32_t>(V);
+  *flag = c.take<char>(V);
+  *cnt = c.take<int64_t>(1);
+  *tb = 0;
+  GB_CUDA_TRY(cub::DeviceSelect::Flagged(nullptr, *tb, (int32_t *)nullptr, (char *)nullptr,
+                                         (int32_t *)nullptr, (int64_t *)nullptr, V));
+  *tmp = c.take_bytes(*tb);
+  return GB_OK;
+}
+
+GB_API int gb_active_sources_workspace(int64_t num_vertices, size_t *bytes) {
+  GB_REQUIRE(num_vertices >= 1 && num_vertices < (int64_t(1) << 31) && bytes,
+             "gb_active_sources_workspace: bad args");
+  Carver c(nullptr);
+  int32_t *ids;
+  char *flag;
+  int64_t *cnt;
+  void *tmp;
+  size_t tb;
+  int rc = active_layout(c, num_vertices, &ids, &flag, &cnt, &tmp, &tb);
+  if (rc) return rc;
+  *bytes = c.off + 256;
+  return GB_OK;
+}
+
+GB_API int gb_active_sources(int64_t num_vertices, const int64_t *xadj, int32_t *out,
+                             int64_t *count_out, void *workspace, size_t ws_bytes,
+                             void *stream_handle) {
+  GB_REQUIRE(num_vertices >= 1 && xadj && out && count_out, "gb_active_sources: bad args");
+  cudaStream_t st = as_stream(stream_handle);
+  Carver c(workspace);
+  int32_t *ids;
+  char *flag;
+  int64_t *cnt;
+  void *tmp;
+  size_t tb;
+  int rc = active_layout(c, num_vertices, &ids, &flag, &cnt, &tmp, &tb);
+  if (rc) return rc;
+  GB_REQUIRE(c.off <= ws_bytes, "gb_active_sources: workspace too small");
+  active_flags<<<blocks_for(num_vertices), 256, 0, st>>>(xadj, num_vertices, ids, flag);
+  GB_CHECK_LAUNCH();
+  GB_CUDA_TRY(cub::DeviceSelect::Flagged(tmp, tb, ids, flag, out, cnt, num_vertices, st));
+  int64_t n = 0;
+  GB_CUDA_TRY(cudaMemcpyAsync(&n, cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GB_CUDA_TRY(cudaStreamSynchronize(st));
+  *count_out = n;
   return GB_OK;
 }

@@ -100,7 +100,7 @@ using namespace gb;
 using namespace gb::tk;
 
 GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int32_t *adj,
-                               float *M, int dim, int n_neg, uint64_t seed, uint64_t rng_stream,
+                               const int32_t *sources, int64_t n_sources, float *M, int dim, int n_neg, uint64_t seed, uint64_t rng_stream,
                                int64_t pass_begin, int64_t n_passes, int64_t passes_per_epoch,
                                const float *lr_per_epoch, unsigned flags, int64_t max_groups,
                                int64_t *status, void *stream_handle) {
@@ -113,12 +113,14 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
   Variant var;
   GB_REQUIRE(pick_variant(dim, aligned16(M, dim), exact, var),
              "gb_train_passes: dim %d unsupported", dim);
-  PassArgs a{num_vertices, xadj, adj, M, dim, n_neg, seed, rng_stream, pass_begin, n_passes,
+  GB_REQUIRE(!sources || n_sources >= 0, "gb_train_passes: bad source list");
+  PassArgs a{num_vertices, xadj, adj, sources, n_sources, M, dim, n_neg, seed, rng_stream, pass_begin, n_passes,
              passes_per_epoch, lr_per_epoch, (flags & GB_TRAIN_REUSE) != 0,
              exact ? 1 : max_groups, status};
   int grid = 1;
   if (!exact) {
-    int rc = grid_for((const void *)var.pass, var.G, max_groups, num_vertices, &grid);
+    int rc = grid_for((const void *)var.pass, var.G, max_groups,
+                      sources ? n_sources : num_vertices, &grid);
     if (rc) return rc;
   }
   var.pass<<<grid, kBlock, 0, as_stream(stream_handle)>>>(a);

@@ -37,10 +37,14 @@ constexpr double kClamp = 10.0;  // SIGMOID_CLAMP, trainer.py:35
 
 // dim == 4*G*NV: lane l holds float4 number k*G + l (k < NV); fully coalesced
 // 16-byte accesses, one 128-byte line per 8 lanes.
+// kMinBlocks: resident 256-thread blocks per SM the register budget targets.
+constexpr int min_blocks_for(int elems) { return elems >= 16 ? 2 : (elems >= 8 ? 3 : 4); }
+
 template <int G_, int NV>
 struct VecRow {
   static constexpr int G = G_;
   static constexpr int E = 4 * NV;
+  static constexpr int kMinBlocks = min_blocks_for(E);
   float x[E];
   __device__ __forceinline__ static bool valid(int, int, int) { return true; }
   __device__ __forceinline__ void load(const float *row, int gl, int) {
@@ -86,6 +90,7 @@ template <int NS>
 struct ScalarRow {
   static constexpr int G = 32;
   static constexpr int E = NS;
+  static constexpr int kMinBlocks = min_blocks_for(NS);
   float x[E];
   __device__ __forceinline__ static bool valid(int k, int gl, int dim) { return k * 32 + gl < dim; }
   __device__ __forceinline__ void load(const float *row, int gl, int dim) {
@@ -199,37 +204,61 @@ __device__ __forceinline__ GroupCtx group_ctx() {
 }
 
 // Runs one chunk of up to kChunk samples against the register-resident
-// source S.  ids[j] < 0 marks an unused slot.  Sample rows are gathered first,
-// then updated in order with forwarding, and stored immediately.
+// source S.  ids[j] < 0 marks an unused slot; bit j of pos_mask marks a
+// positive (b = 1).  Sample rows are gathered first, then updated in order
+// with forwarding of repeated ids, and stored right after their update.
 template <class Row, bool EXACT>
-__device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int64_t (&ids)[kChunk],
-                                          const double (&bs)[kChunk], float *__restrict__ Mtgt,
-                                          int dim, double lr, bool reuse, bool self_possible,
+__device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t (&ids)[kChunk],
+                                          unsigned pos_mask, float *__restrict__ Mtgt, int dim,
+                                          double lr, bool reuse, bool self_possible,
                                           bool load_once, const GroupCtx &g, bool &bad) {
   Row R[kChunk];
 #pragma unroll
   for (int j = 0; j < kChunk; ++j)
     if (ids[j] >= 0 && !(self_possible && ids[j] == src_row))
-      R[j].load(Mtgt + ids[j] * (int64_t)dim, g.gl, dim);
+      R[j].load(Mtgt + (int64_t)ids[j] * dim, g.gl, dim);
 #pragma unroll
   for (int j = 0; j < kChunk; ++j) {
-    const int64_t s = ids[j];
+    const int32_t s = ids[j];
     if (s < 0) continue;
+    const double b = (pos_mask >> j) & 1u ? 1.0 : 0.0;
     if (self_possible && s == src_row) {
       double acc = row_dot<Row, EXACT>(S, S, g.gmask, g.gl, dim);
-      float sc = nce_score(acc, bs[j], lr, bad);
+      float sc = nce_score(acc, b, lr, bad);
       update_self(S, sc, reuse, load_once);
       continue;
     }
     double acc = row_dot<Row, EXACT>(S, R[j], g.gmask, g.gl, dim);
-    float sc = nce_score(acc, bs[j], lr, bad);
+    float sc = nce_score(acc, b, lr, bad);
     update_pair(S, R[j], sc, reuse);
 #pragma unroll
     for (int jj = j + 1; jj < kChunk; ++jj)
       if (ids[jj] == s) R[jj] = R[j];
-    R[j].store(Mtgt + s * (int64_t)dim, g.gl, dim);
+    R[j].store(Mtgt + (int64_t)s * dim, g.gl, dim);
   }
 }
+
+// Work slots.  Group `gid` (slot g of warp w; gpw = 32/G groups per warp) of
+// the `eff` enabled groups handles items gid, gid + eff, ...  The loop bound
+// `base` is the same for every group of a warp, so the groups of a warp walk
+// their items in lockstep and stay converged.
+template <class Row>
+struct Slots {
+  int64_t warp_base;  // gid of the warp's first group
+  int64_t gid;
+  int64_t eff;
+  bool enabled;
+  __device__ __forceinline__ Slots(int64_t max_groups) {
+    constexpr int gpw = 32 / Row::G;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t total = ((int64_t)gridDim.x * blockDim.x >> 5) * gpw;
+    eff = max_groups > 0 ? min(total, max_groups) : total;
+    warp_base = warp * gpw;
+    gid = warp_base + (threadIdx.x & 31) / Row::G;
+    enabled = gid < eff;
+  }
+  __device__ __forceinline__ bool warp_idle() const { return warp_base >= eff; }
+};
 
 // ---------------------------------------------------------------------------
 // In-memory passes (trainer.py:184-207).
@@ -238,6 +267,8 @@ struct PassArgs {
   int64_t V;
   const int64_t *__restrict__ xadj;
   const int32_t *__restrict__ adj;
+  const int32_t *__restrict__ sources;  // non-isolated vertices, ascending (may be null)
+  int64_t n_sources;
   float *M;
   int dim;
   int n_neg;
@@ -253,20 +284,22 @@ struct PassArgs {
 };
 
 template <class Row, bool EXACT>
-__global__ void __launch_bounds__(kBlock) train_passes_kernel(PassArgs a) {
+__global__ void __launch_bounds__(kBlock, Row::kMinBlocks) train_passes_kernel(PassArgs a) {
   const GroupCtx g = group_ctx<Row>();
-  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / Row::G;
-  const int64_t ngroups =
-      min((int64_t)gridDim.x * blockDim.x / Row::G, a.max_groups > 0 ? a.max_groups : INT64_MAX);
-  if (gid >= ngroups) return;  // whole groups leave together
+  const Slots<Row> sl(a.max_groups);
+  if (sl.warp_idle()) return;
   bool bad = false;
   int64_t first_bad = INT64_MAX;
   const int nsamp = 1 + a.n_neg;
+  const int64_t n = a.sources ? a.n_sources : a.V;
 
   for (int64_t p = a.pass_begin; p < a.pass_begin + a.n_passes; ++p) {
     const int64_t epoch = p / a.ppe;
     const double lr = (double)a.lr[epoch];
-    for (int64_t v = gid; v < a.V; v += ngroups) {
+    for (int64_t base = sl.warp_base; base < n; base += sl.eff) {
+      const int64_t i = base + (sl.gid - sl.warp_base);
+      if (!sl.enabled || i >= n) continue;
+      const int64_t v = a.sources ? (int64_t)__ldg(a.sources + i) : i;
       const int64_t x0 = __ldg(a.xadj + v);
       const int64_t deg = __ldg(a.xadj + v + 1) - x0;
       if (deg == 0) continue;  // isolated sources are skipped (trainer.py:198-200)
@@ -275,21 +308,19 @@ __global__ void __launch_bounds__(kBlock) train_passes_kernel(PassArgs a) {
       S.load(a.M + v * (int64_t)a.dim, g.gl, a.dim);
       bool bad_src = false;
       for (int c0 = 0; c0 < nsamp; c0 += kChunk) {
-        int64_t ids[kChunk];
-        double bs[kChunk];
+        int32_t ids[kChunk];
 #pragma unroll
         for (int j = 0; j < kChunk; ++j) {
           const int idx = c0 + j;
-          if (idx >= nsamp) {
+          if (idx >= nsamp)
             ids[j] = -1;
-          } else if (idx == 0) {  // positive: uniform neighbour (trainer.py:203)
+          else if (idx == 0)  // positive: uniform neighbour (trainer.py:203)
             ids[j] = __ldg(a.adj + x0 + draw_below(key, 0, deg));
-          } else {  // negatives: uniform over V (trainer.py:205-206)
-            ids[j] = draw_below(key, (uint64_t)idx, a.V);
-          }
-          bs[j] = idx == 0 ? 1.0 : 0.0;
+          else  // negatives: uniform over V (trainer.py:205-206)
+            ids[j] = (int32_t)draw_below(key, (uint64_t)idx, a.V);
         }
-        run_chunk<Row, EXACT>(S, v, ids, bs, a.M, a.dim, lr, a.reuse, true, false, g, bad_src);
+        run_chunk<Row, EXACT>(S, v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, a.reuse, true,
+                              false, g, bad_src);
       }
       S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
       if (bad_src) {
@@ -344,19 +375,19 @@ __device__ __forceinline__ int64_t lower_bound_adj(const int32_t *__restrict__ a
 }
 
 template <class Row, bool EXACT>
-__global__ void __launch_bounds__(kBlock) train_pool_kernel(PoolArgs a) {
+__global__ void __launch_bounds__(kBlock, Row::kMinBlocks) train_pool_kernel(PoolArgs a) {
   const GroupCtx g = group_ctx<Row>();
-  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / Row::G;
-  const int64_t ngroups =
-      min((int64_t)gridDim.x * blockDim.x / Row::G, a.max_groups > 0 ? a.max_groups : INT64_MAX);
-  if (gid >= ngroups) return;
+  const Slots<Row> sl(a.max_groups);
+  if (sl.warp_idle()) return;
   const bool diagonal = a.Msrc == a.Mtgt;
   const int per_t = 1 + a.n_neg;
   const int64_t total = (int64_t)a.B * per_t;
   bool bad = false;
   unsigned long long pos_count = 0;
 
-  for (int64_t i = gid; i < a.n_src; i += ngroups) {
+  for (int64_t base = sl.warp_base; base < a.n_src; base += sl.eff) {
+    const int64_t i = base + (sl.gid - sl.warp_base);
+    if (!sl.enabled || i >= a.n_src) continue;
     // pool side of this source: either the materialized row or the fused draw
     int64_t first = 0, cnt = 0;
     uint64_t pkey = 0;
@@ -372,14 +403,12 @@ __global__ void __launch_bounds__(kBlock) train_pool_kernel(PoolArgs a) {
     Row S;
     bool loaded = false;
     for (int64_t c0 = 0; c0 < total; c0 += kChunk) {
-      int64_t ids[kChunk];
-      double bs[kChunk];
-      bool any = false;
+      int32_t ids[kChunk];
+      unsigned pos_mask = 0;
 #pragma unroll
       for (int j = 0; j < kChunk; ++j) {
         const int64_t idx = c0 + j;
         ids[j] = -1;
-        bs[j] = 0.0;
         if (idx >= total) continue;
         const int64_t t = idx / per_t;
         const int q = (int)(idx - t * per_t);
@@ -390,21 +419,20 @@ __global__ void __launch_bounds__(kBlock) train_pool_kernel(PoolArgs a) {
           tgt = __ldg(a.adj + first + draw_below(pkey, (uint64_t)t, cnt));
         if (tgt < 0) continue;  // absent slot: no positive, no negatives
         if (q == 0) {
-          ids[j] = tgt - a.lo_t;
-          bs[j] = 1.0;
+          ids[j] = (int32_t)(tgt - a.lo_t);
+          pos_mask |= 1u << j;
         } else {
-          ids[j] = draw_below(key, (uint64_t)(t * a.n_neg + (q - 1)), a.n_t);
+          ids[j] = (int32_t)draw_below(key, (uint64_t)(t * a.n_neg + (q - 1)), a.n_t);
         }
-        any = true;
       }
-      if (!any) continue;
+      if (!(ids[0] >= 0 || ids[1] >= 0 || ids[2] >= 0 || ids[3] >= 0)) continue;
       if (!loaded) {
         S.load(a.Msrc + i * (int64_t)a.dim, g.gl, a.dim);
         loaded = true;
       }
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) pos_count += (ids[j] >= 0 && bs[j] == 1.0) ? 1 : 0;
-      run_chunk<Row, EXACT>(S, i, ids, bs, a.Mtgt, a.dim, a.lr, a.reuse, diagonal, true, g, bad);
+      pos_count += __popc(pos_mask);
+      run_chunk<Row, EXACT>(S, i, ids, pos_mask, a.Mtgt, a.dim, a.lr, a.reuse, diagonal, true,
+                            g, bad);
     }
     if (loaded) S.store(a.Msrc + i * (int64_t)a.dim, g.gl, a.dim);
   }
@@ -437,27 +465,27 @@ struct ListArgs {
 };
 
 template <class Row, bool EXACT>
-__global__ void __launch_bounds__(kBlock) apply_lists_kernel(ListArgs a) {
+__global__ void __launch_bounds__(kBlock, Row::kMinBlocks) apply_lists_kernel(ListArgs a) {
   const GroupCtx g = group_ctx<Row>();
-  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / Row::G;
-  const int64_t ngroups =
-      min((int64_t)gridDim.x * blockDim.x / Row::G, a.max_groups > 0 ? a.max_groups : INT64_MAX);
-  if (gid >= ngroups) return;
+  const Slots<Row> sl(a.max_groups);
+  if (sl.warp_idle()) return;
   bool bad = false;
-  for (int64_t i = gid; i < a.n_src; i += ngroups) {
+  for (int64_t base = sl.warp_base; base < a.n_src; base += sl.eff) {
+    const int64_t i = base + (sl.gid - sl.warp_base);
+    if (!sl.enabled || i >= a.n_src) continue;
     const int64_t v = a.src[i];
     Row S;
     S.load(a.M + v * (int64_t)a.dim, g.gl, a.dim);
     for (int c0 = 0; c0 < a.k; c0 += kChunk) {
-      int64_t ids[kChunk];
-      double bs[kChunk];
+      int32_t ids[kChunk];
+      unsigned pos_mask = 0;
 #pragma unroll
       for (int j = 0; j < kChunk; ++j) {
         const int idx = c0 + j;
-        ids[j] = idx < a.k ? a.samples[i * a.k + idx] : -1;
-        bs[j] = idx < a.k ? (double)a.labels[idx] : 0.0;
+        ids[j] = idx < a.k ? (int32_t)a.samples[i * a.k + idx] : -1;
+        if (idx < a.k && a.labels[idx]) pos_mask |= 1u << j;
       }
-      run_chunk<Row, EXACT>(S, v, ids, bs, a.M, a.dim, a.lr, a.reuse, true, false, g, bad);
+      run_chunk<Row, EXACT>(S, v, ids, pos_mask, a.M, a.dim, a.lr, a.reuse, true, false, g, bad);
     }
     S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
   }

@@ -89,6 +89,21 @@ class Graph:
             self._adj_dev = torch.from_numpy(a).cuda()
         return self._xadj_dev, self._adj_dev
 
+    def active_sources(self) -> tuple[torch.Tensor, int]:
+        """Non-isolated vertex ids (int32, ascending) -- the sources a
+        training pass visits (trainer.py:198-200); computed once on the GPU."""
+        cached = getattr(self, "_active", None)
+        if cached is None:
+            xadj, _ = self.device_csr()
+            ws, wsb = _lib.workspace("gb_active_sources_workspace", self.num_vertices)
+            out = torch.empty(self.num_vertices, dtype=torch.int32, device="cuda")
+            n = C.c_int64(0)
+            _lib.call("gb_active_sources", self.num_vertices, _lib.ptr(xadj), _lib.ptr(out),
+                      C.byref(n), _lib.ptr(ws), wsb, _lib.stream())
+            cached = (out[: max(int(n.value), 1)].clone(), int(n.value))
+            self._active = cached
+        return cached
+
     def drop_host(self) -> None:
         """Forget the host copies of a device-resident graph."""
         if self._xadj_dev is not None:

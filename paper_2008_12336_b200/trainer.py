@@ -276,6 +276,7 @@ def train_level(g: Graph, M, cfg: TrainConfig, e_i: int, lr0: float | None = Non
         return TrainStats(passes=0, updates=0)
     dm = _DeviceMatrix(M)
     xadj, adj = g.device_csr()
+    sources, n_src = g.active_sources()
     lrs = torch.tensor([float(np.float32(lr_at(lr0, j, e_i))) for j in range(e_i)],
                        dtype=torch.float32, device="cuda")
     status = _lib.new_status()
@@ -284,7 +285,7 @@ def train_level(g: Graph, M, cfg: TrainConfig, e_i: int, lr0: float | None = Non
     st = _lib.stream()
     for j in range(e_i):
         _lib.call("gb_train_passes", g.num_vertices, _lib.ptr(xadj), _lib.ptr(adj),
-                  _lib.ptr(dm.dev), cfg.dim, cfg.negative_samples, _lib.u64(cfg.seed),
+                  _lib.ptr(sources), n_src, _lib.ptr(dm.dev), cfg.dim, cfg.negative_samples, _lib.u64(cfg.seed),
                   _lib.u64(rng_stream), j * ppe, ppe, ppe, _lib.ptr(lrs), flags, cap,
                   _lib.ptr(status), st)
     _lib.call("gb_nonfinite_scan", _lib.ptr(dm.dev), dm.dev.numel(), e_i - 1, _lib.ptr(status),
@@ -292,8 +293,7 @@ def train_level(g: Graph, M, cfg: TrainConfig, e_i: int, lr0: float | None = Non
     dm.close()
     _raise_if_nonfinite(status, "epoch")
     passes = e_i * ppe
-    return TrainStats(passes=passes,
-                      updates=passes * _non_isolated(g) * (1 + cfg.negative_samples))
+    return TrainStats(passes=passes, updates=passes * n_src * (1 + cfg.negative_samples))
 
 
 def expand_embedding(M_next, m: Mapping):

@@ -186,7 +186,9 @@ def test_train_pass_exact_bit_exact_vs_reference(cuda, golden):
         st = _lib.new_status()
         x, a = G.device_csr()
         flags = _lib.GB_TRAIN_EXACT | (_lib.GB_TRAIN_REUSE if reuse else 0)
-        _lib.call("gb_train_passes", G.num_vertices, _lib.ptr(x), _lib.ptr(a), _lib.ptr(M),
+        src, n_src = G.active_sources() if k % 2 else (None, 0)
+        _lib.call("gb_train_passes", G.num_vertices, _lib.ptr(x), _lib.ptr(a), _lib.ptr(src),
+                  n_src, _lib.ptr(M),
                   int(d), int(n_neg), int(seed), int(stream), 0, 3, 1, _lib.ptr(lrs), flags, 1,
                   _lib.ptr(st), _lib.stream())
         assert np.array_equal(M.cpu().numpy(), g[f"c{k}_M3"]), k

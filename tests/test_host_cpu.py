@@ -38,7 +38,8 @@ def test_library_exports_every_header_symbol():
 
 def test_library_rejects_bad_arguments_without_gpu():
     L = _lib.load()
-    rc = L.gb_train_passes(10, None, None, None, 0, 3, 1, 0, 0, 1, 1, None, 0, 0, None, None)
+    rc = L.gb_train_passes(10, None, None, None, 0, None, 0, 3, 1, 0, 0, 1, 1, None, 0, 0, None,
+                           None)
     assert rc == _lib.GB_E_INVALID
     assert b"gb_train_passes" in L.gb_last_error()
     with pytest.raises(ValueError):
