@@ -44,6 +44,7 @@ def workload_config(extra=None):
                        "edges, Graph500 a,b,c=0.57,0.19,0.19), d=128, n_neg=3",
            "scale": SCALE, "sampled_edges": SAMPLES, "dim": DIM, "negatives": NNEG,
            "rmat_seed": SEED, "lr": LR, "step": "one vertex pass (1 kernel launch)",
+           "kernel_flags": "default non-deterministic path (fp64 dot, fp32 sigmoid)",
            "l2": "inputs larger than L2 (embedding matrix 512 MiB > 126 MB L2), no flush"}
     if extra:
         cfg.update(extra)
@@ -216,7 +217,8 @@ def run_ours(args):
     def launch(p):
         _lib.call("gb_train_passes", V, _lib.ptr(xadj), _lib.ptr(adj), _lib.ptr(sources),
                   non_iso, _lib.ptr(M), DIM, NNEG,
-                  1, 0, p, 1, 1 << 40, _lib.ptr(lrs), 0, cap, _lib.ptr(status),
+                  1, 0, p, 1, 1 << 40, _lib.ptr(lrs), _lib.GB_TRAIN_FAST_SIGMOID, cap,
+                  _lib.ptr(status),
                   stream.cuda_stream)
 
     for p in range(args.warmup):

@@ -116,14 +116,36 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
   GB_REQUIRE(!sources || n_sources >= 0, "gb_train_passes: bad source list");
   PassArgs a{num_vertices, xadj, adj, sources, n_sources, M, dim, n_neg, seed, rng_stream, pass_begin, n_passes,
              passes_per_epoch, lr_per_epoch, (flags & GB_TRAIN_REUSE) != 0,
-             exact ? 1 : max_groups, status};
-  int grid = 1;
+             (flags & GB_TRAIN_FAST_SIGMOID) != 0, exact ? 1 : max_groups, status};
+  int grid = 1, block = kBlock;
+  PassFn fn = var.pass;
   if (!exact) {
-    int rc = grid_for((const void *)var.pass, var.G, max_groups,
-                      sources ? n_sources : num_vertices, &grid);
+    const int64_t items = sources ? n_sources : num_vertices;
+    int rc = grid_for((const void *)var.pass, var.G, max_groups, items, &grid);
     if (rc) return rc;
+    // a launch capped below full occupancy is latency-bound: use the
+    // prefetching variant (GB_PIPE=0/1 forces the choice for experiments)
+    int occ = 0;
+    GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)var.pass,
+                                                              kBlock, 0));
+    bool pipe = (int64_t)grid < (int64_t)num_sms() * std::max(occ, 1);
+    if (const char *env = std::getenv("GB_PIPE")) pipe = std::atoi(env) != 0;
+    if (pipe) {
+      // latency-bound: one warp per block so the capped groups spread over
+      // as many SMs as possible instead of sharing a few
+      fn = var.pass_pipe;
+      const int64_t gpw = 32 / var.G;
+      const int64_t groups = std::min<int64_t>(max_groups > 0 ? max_groups : INT64_MAX, items);
+      const int64_t warps = std::max<int64_t>(1, (groups + gpw - 1) / gpw);
+      int occ1 = 0;
+      GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, (const void *)fn, 32, 0));
+      grid = (int)std::min<int64_t>(warps, (int64_t)num_sms() * std::max(occ1, 1));
+      block = 32;
+    }
+  } else {
+    block = 32;
   }
-  var.pass<<<grid, kBlock, 0, as_stream(stream_handle)>>>(a);
+  fn<<<grid, block, 0, as_stream(stream_handle)>>>(a);
   GB_CHECK_LAUNCH();
   return GB_OK;
 }
@@ -144,7 +166,8 @@ GB_API int gb_train_pool_side(float *Msrc, float *Mtgt, int dim, const int32_t *
   GB_REQUIRE(pick_variant(dim, aligned16(Msrc, dim) && aligned16(Mtgt, dim), exact, var),
              "gb_train_pool_side: dim %d unsupported", dim);
   PoolArgs a{Msrc, Mtgt, dim, targets, n_src, B, lo_t, n_t, n_neg, lr, seed, side, xadj, adj,
-             lo_s, pool_side, (flags & GB_TRAIN_REUSE) != 0, exact ? 1 : max_groups, status};
+             lo_s, pool_side, (flags & GB_TRAIN_REUSE) != 0,
+             (flags & GB_TRAIN_FAST_SIGMOID) != 0, exact ? 1 : max_groups, status};
   int grid = 1;
   if (!exact) {
     int rc = grid_for((const void *)var.pool, var.G, max_groups, n_src, &grid);
@@ -179,7 +202,7 @@ GB_API int gb_apply_sample_lists(float *M, int dim, int64_t n_src, const int64_t
   GB_REQUIRE(pick_variant(dim, aligned16(M, dim), exact, var),
              "gb_apply_sample_lists: dim %d unsupported", dim);
   ListArgs a{M, dim, n_src, src, k, samples, labels, lr, (flags & GB_TRAIN_REUSE) != 0,
-             exact ? 1 : max_groups, status};
+             (flags & GB_TRAIN_FAST_SIGMOID) != 0, exact ? 1 : max_groups, status};
   int grid = 1;
   if (!exact) {
     int rc = grid_for((const void *)var.lists, var.G, max_groups, n_src, &grid);

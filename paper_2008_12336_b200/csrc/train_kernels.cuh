@@ -124,23 +124,41 @@ template <class Row, bool EXACT>
 __device__ __forceinline__ double row_dot(const Row &a, const Row &b, unsigned gmask, int gl,
                                           int dim) {
   if (EXACT) return Row::serial_dot(a, b, gmask, gl, dim);
-  double part = 0.0;
+  double p0 = 0.0, p1 = 0.0;  // two chains: halves the dependent DFMA latency
 #pragma unroll
   for (int k = 0; k < Row::E; ++k)
-    if (Row::valid(k, gl, dim)) part = __fma_rn((double)a.x[k], (double)b.x[k], part);
+    if (Row::valid(k, gl, dim)) {
+      if (k & 1)
+        p1 = __fma_rn((double)a.x[k], (double)b.x[k], p1);
+      else
+        p0 = __fma_rn((double)a.x[k], (double)b.x[k], p0);
+    }
+  double part = __dadd_rn(p0, p1);
 #pragma unroll
   for (int off = Row::G / 2; off > 0; off >>= 1)
     part = __dadd_rn(part, __shfl_xor_sync(gmask, part, off, Row::G));
   return part;
 }
 
-// score = f32((b - sigmoid(clamp(acc))) * lr)   (trainer.py:124-130)
-__device__ __forceinline__ float nce_score(double acc, double b, double lr, bool &bad) {
+// score = f32((b - sigmoid(clamp(acc))) * lr)   (trainer.py:124-130).
+// fast (non-exact kernels only): the same quantity in fp32 without the
+// cancellation of b - sigmoid: lr*sigmoid(-x) for b=1, -lr*sigmoid(x) for
+// b=0 (relative error ~1e-7; the fp64 dot is kept).  Cuts the per-update
+// dependency chain by the fp64 exp + divide.
+__device__ __forceinline__ float nce_score(double acc, double b, double lr, bool &bad,
+                                           bool fast = false) {
   bad |= !isfinite(acc);
   if (acc > kClamp)
     acc = kClamp;
   else if (acc < -kClamp)
     acc = -kClamp;
+  if (fast) {
+    const float x = __double2float_rn(acc);
+    const bool positive = b != 0.0;
+    const float s = __fdividef(1.0f, 1.0f + expf(positive ? x : -x));
+    const float l = __double2float_rn(lr);
+    return positive ? s * l : -s * l;
+  }
   double sig = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-acc)));
   return __double2float_rn(__dmul_rn(__dsub_rn(b, sig), lr));
 }
@@ -211,7 +229,8 @@ template <class Row, bool EXACT>
 __device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t (&ids)[kChunk],
                                           unsigned pos_mask, float *__restrict__ Mtgt, int dim,
                                           double lr, bool reuse, bool self_possible,
-                                          bool load_once, const GroupCtx &g, bool &bad) {
+                                          bool load_once, const GroupCtx &g, bool &bad,
+                                          bool fast = false) {
   Row R[kChunk];
 #pragma unroll
   for (int j = 0; j < kChunk; ++j)
@@ -224,12 +243,12 @@ __device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t
     const double b = (pos_mask >> j) & 1u ? 1.0 : 0.0;
     if (self_possible && s == src_row) {
       double acc = row_dot<Row, EXACT>(S, S, g.gmask, g.gl, dim);
-      float sc = nce_score(acc, b, lr, bad);
+      float sc = nce_score(acc, b, lr, bad, fast && !EXACT);
       update_self(S, sc, reuse, load_once);
       continue;
     }
     double acc = row_dot<Row, EXACT>(S, R[j], g.gmask, g.gl, dim);
-    float sc = nce_score(acc, b, lr, bad);
+    float sc = nce_score(acc, b, lr, bad, fast && !EXACT);
     update_pair(S, R[j], sc, reuse);
 #pragma unroll
     for (int jj = j + 1; jj < kChunk; ++jj)
@@ -279,54 +298,148 @@ struct PassArgs {
   int64_t ppe;
   const float *__restrict__ lr;
   bool reuse;
+  bool fast;
   int64_t max_groups;
   int64_t *status;
 };
 
+// Index half of a source (read-only data: xadj, adj, the RNG) -- prefetched
+// one source ahead so the xadj -> adj -> positive-id chain overlaps the
+// previous source's row updates.  Prefetching it does not change results.
+struct SourceIdx {
+  int64_t v;
+  int64_t x0;
+  int64_t deg;
+  uint64_t key;
+  int32_t ids[kChunk];  // first chunk: positive + up to kChunk-1 negatives
+  bool active;
+};
+
+__device__ __forceinline__ void fetch_source(const PassArgs &a, int64_t p, int64_t i, bool ok,
+                                             SourceIdx &d) {
+  d.active = ok;
+  if (!ok) return;
+  d.v = a.sources ? (int64_t)__ldg(a.sources + i) : i;
+  d.x0 = __ldg(a.xadj + d.v);
+  d.deg = __ldg(a.xadj + d.v + 1) - d.x0;
+  if (d.deg == 0) {  // isolated sources are skipped (trainer.py:198-200)
+    d.active = false;
+    return;
+  }
+  d.key = stream_key(a.seed, a.stream, (uint64_t)p, (uint64_t)d.v);
+  const int nsamp = 1 + a.n_neg;
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) {
+    if (j >= nsamp)
+      d.ids[j] = -1;
+    else if (j == 0)  // positive: uniform neighbour (trainer.py:203)
+      d.ids[j] = __ldg(a.adj + d.x0 + draw_below(d.key, 0, d.deg));
+    else  // negatives: uniform over V (trainer.py:205-206)
+      d.ids[j] = (int32_t)draw_below(d.key, (uint64_t)j, a.V);
+  }
+}
+
+// Processes one source whose index half is in `d` (run_chunk per chunk).
 template <class Row, bool EXACT>
-__global__ void __launch_bounds__(kBlock, Row::kMinBlocks) train_passes_kernel(PassArgs a) {
+__device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &g,
+                                             const SourceIdx &d, int64_t p, bool &bad,
+                                             int64_t &first_bad) {
+  const int nsamp = 1 + a.n_neg;
+  const int64_t epoch = p / a.ppe;
+  const double lr = (double)__ldg(a.lr + epoch);
+  Row S;
+  S.load(a.M + d.v * (int64_t)a.dim, g.gl, a.dim);
+  bool bad_src = false;
+  run_chunk<Row, EXACT>(S, d.v, d.ids, 1u, a.M, a.dim, lr, a.reuse, true, false, g, bad_src,
+                        a.fast);
+  for (int c0 = kChunk; c0 < nsamp; c0 += kChunk) {  // only when n_neg >= kChunk
+    int32_t ids[kChunk];
+#pragma unroll
+    for (int j = 0; j < kChunk; ++j)
+      ids[j] = c0 + j < nsamp ? (int32_t)draw_below(d.key, (uint64_t)(c0 + j), a.V) : -1;
+    run_chunk<Row, EXACT>(S, d.v, ids, 0u, a.M, a.dim, lr, a.reuse, true, false, g, bad_src,
+                          a.fast);
+  }
+  S.store(a.M + d.v * (int64_t)a.dim, g.gl, a.dim);
+  if (bad_src) {
+    bad = true;
+    first_bad = min(first_bad, epoch);
+  }
+}
+
+// PIPE = false: throughput variant for full-occupancy (HBM-bound) launches.
+// PIPE = true: latency variant for capped launches on small levels -- the
+// index half of the next source is fetched before the current source's row
+// updates (more registers, one block per SM is plenty there).
+template <class Row, bool EXACT, bool PIPE>
+__global__ void __launch_bounds__(kBlock, PIPE ? 1 : Row::kMinBlocks)
+    train_passes_kernel(PassArgs a) {
   const GroupCtx g = group_ctx<Row>();
   const Slots<Row> sl(a.max_groups);
   if (sl.warp_idle()) return;
   bool bad = false;
   int64_t first_bad = INT64_MAX;
-  const int nsamp = 1 + a.n_neg;
   const int64_t n = a.sources ? a.n_sources : a.V;
-
-  for (int64_t p = a.pass_begin; p < a.pass_begin + a.n_passes; ++p) {
-    const int64_t epoch = p / a.ppe;
-    const double lr = (double)a.lr[epoch];
-    for (int64_t base = sl.warp_base; base < n; base += sl.eff) {
-      const int64_t i = base + (sl.gid - sl.warp_base);
-      if (!sl.enabled || i >= n) continue;
-      const int64_t v = a.sources ? (int64_t)__ldg(a.sources + i) : i;
-      const int64_t x0 = __ldg(a.xadj + v);
-      const int64_t deg = __ldg(a.xadj + v + 1) - x0;
-      if (deg == 0) continue;  // isolated sources are skipped (trainer.py:198-200)
-      const uint64_t key = stream_key(a.seed, a.stream, (uint64_t)p, (uint64_t)v);
-      Row S;
-      S.load(a.M + v * (int64_t)a.dim, g.gl, a.dim);
-      bool bad_src = false;
-      for (int c0 = 0; c0 < nsamp; c0 += kChunk) {
-        int32_t ids[kChunk];
+  const int64_t lane_off = sl.gid - sl.warp_base;
+  if constexpr (!PIPE) {
+    const int nsamp = 1 + a.n_neg;
+    for (int64_t p = a.pass_begin; p < a.pass_begin + a.n_passes; ++p) {
+      const int64_t epoch = p / a.ppe;
+      const double lr = (double)__ldg(a.lr + epoch);
+      for (int64_t base = sl.warp_base; base < n; base += sl.eff) {
+        const int64_t i = base + lane_off;
+        if (!sl.enabled || i >= n) continue;
+        const int64_t v = a.sources ? (int64_t)__ldg(a.sources + i) : i;
+        const int64_t x0 = __ldg(a.xadj + v);
+        const int64_t deg = __ldg(a.xadj + v + 1) - x0;
+        if (deg == 0) continue;  // isolated sources are skipped (trainer.py:198-200)
+        const uint64_t key = stream_key(a.seed, a.stream, (uint64_t)p, (uint64_t)v);
+        Row S;
+        S.load(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+        bool bad_src = false;
+        for (int c0 = 0; c0 < nsamp; c0 += kChunk) {
+          int32_t ids[kChunk];
 #pragma unroll
-        for (int j = 0; j < kChunk; ++j) {
-          const int idx = c0 + j;
-          if (idx >= nsamp)
-            ids[j] = -1;
-          else if (idx == 0)  // positive: uniform neighbour (trainer.py:203)
-            ids[j] = __ldg(a.adj + x0 + draw_below(key, 0, deg));
-          else  // negatives: uniform over V (trainer.py:205-206)
-            ids[j] = (int32_t)draw_below(key, (uint64_t)idx, a.V);
+          for (int j = 0; j < kChunk; ++j) {
+            const int idx = c0 + j;
+            if (idx >= nsamp)
+              ids[j] = -1;
+            else if (idx == 0)  // positive: uniform neighbour (trainer.py:203)
+              ids[j] = __ldg(a.adj + x0 + draw_below(key, 0, deg));
+            else  // negatives: uniform over V (trainer.py:205-206)
+              ids[j] = (int32_t)draw_below(key, (uint64_t)idx, a.V);
+          }
+          run_chunk<Row, EXACT>(S, v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, a.reuse, true,
+                                false, g, bad_src, a.fast);
         }
-        run_chunk<Row, EXACT>(S, v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, a.reuse, true,
-                              false, g, bad_src);
+        S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+        if (bad_src) {
+          bad = true;
+          first_bad = min(first_bad, epoch);
+        }
       }
-      S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
-      if (bad_src) {
-        bad = true;
-        first_bad = min(first_bad, epoch);
+    }
+  } else {
+    // (pass, item) cursor: the warp-uniform `base` advances by eff per step
+    // and wraps into the next pass.
+    const int64_t p_end = a.pass_begin + a.n_passes;
+    int64_t p = a.pass_begin, base = sl.warp_base;
+    if (base >= n) return;
+    SourceIdx cur;
+    fetch_source(a, p, base + lane_off, sl.enabled && base + lane_off < n, cur);
+    while (p < p_end) {
+      int64_t np = p, nbase = base + sl.eff;
+      if (nbase >= n) {
+        ++np;
+        nbase = sl.warp_base;
       }
+      SourceIdx nxt;
+      fetch_source(a, np, nbase + lane_off, np < p_end && sl.enabled && nbase + lane_off < n,
+                   nxt);
+      if (cur.active) train_source<Row, EXACT>(a, g, cur, p, bad, first_bad);
+      cur = nxt;
+      p = np;
+      base = nbase;
     }
   }
   if (bad && g.gl == 0) {
@@ -357,6 +470,7 @@ struct PoolArgs {
   int64_t lo_s;
   uint64_t pool_side;
   bool reuse;
+  bool fast;
   int64_t max_groups;
   int64_t *status;
 };
@@ -432,7 +546,7 @@ __global__ void __launch_bounds__(kBlock, Row::kMinBlocks) train_pool_kernel(Poo
       }
       pos_count += __popc(pos_mask);
       run_chunk<Row, EXACT>(S, i, ids, pos_mask, a.Mtgt, a.dim, a.lr, a.reuse, diagonal, true,
-                            g, bad);
+                            g, bad, a.fast);
     }
     if (loaded) S.store(a.Msrc + i * (int64_t)a.dim, g.gl, a.dim);
   }
@@ -460,6 +574,7 @@ struct ListArgs {
   const int8_t *__restrict__ labels;
   double lr;
   bool reuse;
+  bool fast;
   int64_t max_groups;
   int64_t *status;
 };
@@ -485,7 +600,8 @@ __global__ void __launch_bounds__(kBlock, Row::kMinBlocks) apply_lists_kernel(Li
         ids[j] = idx < a.k ? (int32_t)a.samples[i * a.k + idx] : -1;
         if (idx < a.k && a.labels[idx]) pos_mask |= 1u << j;
       }
-      run_chunk<Row, EXACT>(S, v, ids, pos_mask, a.M, a.dim, a.lr, a.reuse, true, false, g, bad);
+      run_chunk<Row, EXACT>(S, v, ids, pos_mask, a.M, a.dim, a.lr, a.reuse, true, false, g, bad,
+                            a.fast);
     }
     S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
   }
@@ -504,7 +620,8 @@ using ListFn = void (*)(ListArgs);
 
 struct Variant {
   int G = 0;
-  PassFn pass = nullptr;
+  PassFn pass = nullptr;       // throughput (full occupancy)
+  PassFn pass_pipe = nullptr;  // latency (capped launches)
   PoolFn pool = nullptr;
   ListFn lists = nullptr;
 };
@@ -513,7 +630,8 @@ template <class Row, bool EXACT>
 Variant make_variant() {
   Variant v;
   v.G = Row::G;
-  v.pass = train_passes_kernel<Row, EXACT>;
+  v.pass = train_passes_kernel<Row, EXACT, false>;
+  v.pass_pipe = train_passes_kernel<Row, EXACT, true>;
   v.pool = train_pool_kernel<Row, EXACT>;
   v.lists = apply_lists_kernel<Row, EXACT>;
   return v;

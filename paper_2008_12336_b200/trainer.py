@@ -145,9 +145,10 @@ class _DeviceMatrix:
 
 
 def _train_flags(cfg: TrainConfig) -> int:
+    """EXACT kernels when deterministic; otherwise the parallel kernels with
+    the fp32 cancellation-free sigmoid (fp64 dot kept)."""
     flags = _lib.GB_TRAIN_REUSE if cfg.reuse_updated_source else 0
-    if cfg.deterministic:
-        flags |= _lib.GB_TRAIN_EXACT
+    flags |= _lib.GB_TRAIN_EXACT if cfg.deterministic else _lib.GB_TRAIN_FAST_SIGMOID
     return flags
 
 
@@ -194,7 +195,7 @@ def apply_sample_lists(M, sources, samples, labels, lr: float, deterministic: bo
     smp = torch.as_tensor(np.ascontiguousarray(samples, dtype=np.int64)).cuda()
     lab = torch.as_tensor(np.asarray(labels, dtype=np.int8)).cuda()
     k = int(smp.shape[1]) if smp.dim() == 2 else 0
-    flags = (_lib.GB_TRAIN_EXACT if deterministic else 0) | (
+    flags = (_lib.GB_TRAIN_EXACT if deterministic else _lib.GB_TRAIN_FAST_SIGMOID) | (
         _lib.GB_TRAIN_REUSE if reuse_updated_source else 0)
     status = _lib.new_status()
     _lib.call("gb_apply_sample_lists", _lib.ptr(dm.dev), dm.dev.shape[1], int(src.numel()),

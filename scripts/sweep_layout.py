@@ -30,7 +30,7 @@ for g in lanes:
             global p
             _lib.call("gb_train_passes", G.num_vertices, _lib.ptr(xadj), _lib.ptr(adj),
                       _lib.ptr(src), n_src, _lib.ptr(M), dim, 3, 1, 0, p, 1, 1 << 40,
-                      _lib.ptr(lrs), 0, cap, _lib.ptr(st), _lib.stream())
+                      _lib.ptr(lrs), int(os.environ.get('FLAGS', '4')), cap, _lib.ptr(st), _lib.stream())
             p += 1
         for _ in range(3):
             launch()
