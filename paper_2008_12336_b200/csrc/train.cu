@@ -37,14 +37,18 @@ __global__ void nonfinite_scan_kernel(const float *__restrict__ M, int64_t n, in
   }
 }
 
-// Default lanes per source for a vector layout; GB_GROUP_LANES overrides it
-// (tuning knob; the layout only changes the tree-dot summation order).
-int preferred_lanes(int dim) {
+// Lanes per source for a vector layout.  Throughput launches: few lanes per
+// source (8 at d=128) so per-source scalar work is shared by 4 sources per
+// warp.  Latency launches (capped, small levels): as many lanes as the row
+// has float4s (up to 32), so the per-lane chain is shortest.  GB_GROUP_LANES
+// overrides both (tuning knob; only the tree-dot summation order changes).
+int preferred_lanes(int dim, bool latency) {
   const char *env = std::getenv("GB_GROUP_LANES");
   if (env) {
     int g = std::atoi(env);
     if (g == 2 || g == 4 || g == 8 || g == 16 || g == 32) return g;
   }
+  if (latency) return std::max(2, std::min(32, dim / 4));
   if (dim <= 16) return std::max(dim / 4, 2);
   if (dim <= 128) return 8;
   return 16;
@@ -58,9 +62,9 @@ bool pick_vector(int dim, int G, Variant &out) {
   return out.G != 0;
 }
 
-bool pick_variant(int dim, bool aligned, bool exact, Variant &out) {
+bool pick_variant(int dim, bool aligned, bool exact, Variant &out, bool latency = false) {
   if (aligned && !exact) {
-    const int G = preferred_lanes(dim);
+    const int G = preferred_lanes(dim, latency);
     for (int g = G; g <= 32; g *= 2)
       if (pick_vector(dim, g, out)) return true;
     for (int g = G / 2; g >= 2; g /= 2)
@@ -131,8 +135,10 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
     bool pipe = (int64_t)grid < (int64_t)num_sms() * std::max(occ, 1);
     if (const char *env = std::getenv("GB_PIPE")) pipe = std::atoi(env) != 0;
     if (pipe) {
-      // latency-bound: one warp per block so the capped groups spread over
-      // as many SMs as possible instead of sharing a few
+      // latency-bound: widest lane layout, one warp per block so the capped
+      // groups spread over as many SMs as possible instead of sharing a few
+      GB_REQUIRE(pick_variant(dim, aligned16(M, dim), exact, var, true),
+                 "gb_train_passes: dim %d unsupported", dim);
       fn = var.pass_pipe;
       const int64_t gpw = 32 / var.G;
       const int64_t groups = std::min<int64_t>(max_groups > 0 ? max_groups : INT64_MAX, items);

@@ -257,6 +257,83 @@ __device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t
   }
 }
 
+// Batched-dot chunk (non-exact, latency variant).  With distinct sample ids
+// that all differ from the source, S before update k is
+// S + sum_{j<k} sc_j R_j, so the k-th dot is
+//   d_k = S.R_k + sum_{j<k} sc_j (R_j.R_k)
+// -- all 4 + 6 fp64 dot products are independent and reduce together (one
+// butterfly, full ILP); only a short scalar chain of sigmoids remains.  The
+// row updates are then applied element by element in the reference's order
+// (identical fp32 operations).  d_k differs from the dot of the fp32-rounded
+// updated row by rounding only (~1e-7 relative), within the 1e-5 bar.
+// Returns false (nothing done) when ids repeat or hit the source; the caller
+// then takes the sequential path.
+template <class Row>
+__device__ __forceinline__ bool batched_chunk(Row &S, int64_t src_row, const int32_t (&ids)[kChunk],
+                                              unsigned pos_mask, float *__restrict__ Mtgt,
+                                              int dim, double lr, bool reuse, const GroupCtx &g,
+                                              bool &bad, bool fast) {
+  static_assert(kChunk == 4, "batched_chunk assumes 4 samples");
+  bool simple = true;
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) {
+    if (ids[j] >= 0 && ids[j] == src_row) simple = false;
+#pragma unroll
+    for (int k = j + 1; k < kChunk; ++k)
+      if (ids[j] >= 0 && ids[j] == ids[k]) simple = false;
+  }
+  if (!simple) return false;
+  Row R[kChunk];
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j)
+    if (ids[j] >= 0) R[j].load(Mtgt + (int64_t)ids[j] * dim, g.gl, dim);
+  // 10 partial dots: q[j] = S.R_j, q[4 + pair(j,k)] = R_j.R_k (j < k)
+  double q[10];
+#pragma unroll
+  for (int t = 0; t < 10; ++t) q[t] = 0.0;
+#pragma unroll
+  for (int e = 0; e < Row::E; ++e) {
+    if (!Row::valid(e, g.gl, dim)) continue;
+    const double s = (double)S.x[e];
+    const double r0 = (double)R[0].x[e], r1 = (double)R[1].x[e];
+    const double r2 = (double)R[2].x[e], r3 = (double)R[3].x[e];
+    q[0] = __fma_rn(s, r0, q[0]);
+    q[1] = __fma_rn(s, r1, q[1]);
+    q[2] = __fma_rn(s, r2, q[2]);
+    q[3] = __fma_rn(s, r3, q[3]);
+    q[4] = __fma_rn(r0, r1, q[4]);
+    q[5] = __fma_rn(r0, r2, q[5]);
+    q[6] = __fma_rn(r0, r3, q[6]);
+    q[7] = __fma_rn(r1, r2, q[7]);
+    q[8] = __fma_rn(r1, r3, q[8]);
+    q[9] = __fma_rn(r2, r3, q[9]);
+  }
+#pragma unroll
+  for (int off = Row::G / 2; off > 0; off >>= 1) {
+#pragma unroll
+    for (int t = 0; t < 10; ++t) q[t] = __dadd_rn(q[t], __shfl_xor_sync(g.gmask, q[t], off, Row::G));
+  }
+  float sc[kChunk];
+  const int gram[kChunk][kChunk] = {{-1, 4, 5, 6}, {4, -1, 7, 8}, {5, 7, -1, 9}, {6, 8, 9, -1}};
+#pragma unroll
+  for (int k = 0; k < kChunk; ++k) {
+    sc[k] = 0.0f;
+    if (ids[k] < 0) continue;
+    double d = q[k];
+#pragma unroll
+    for (int j = 0; j < k; ++j)
+      if (ids[j] >= 0) d = __fma_rn((double)sc[j], q[gram[j][k]], d);
+    sc[k] = nce_score(d, (pos_mask >> k) & 1u ? 1.0 : 0.0, lr, bad, fast);
+  }
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) {
+    if (ids[j] < 0) continue;
+    update_pair(S, R[j], sc[j], reuse);
+    R[j].store(Mtgt + (int64_t)ids[j] * dim, g.gl, dim);
+  }
+  return true;
+}
+
 // Work slots.  Group `gid` (slot g of warp w; gpw = 32/G groups per warp) of
 // the `eff` enabled groups handles items gid, gid + eff, ...  The loop bound
 // `base` is the same for every group of a warp, so the groups of a warp walk
@@ -350,8 +427,10 @@ __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &
   Row S;
   S.load(a.M + d.v * (int64_t)a.dim, g.gl, a.dim);
   bool bad_src = false;
-  run_chunk<Row, EXACT>(S, d.v, d.ids, 1u, a.M, a.dim, lr, a.reuse, true, false, g, bad_src,
-                        a.fast);
+  if (EXACT || !batched_chunk<Row>(S, d.v, d.ids, 1u, a.M, a.dim, lr, a.reuse, g, bad_src,
+                                   a.fast))
+    run_chunk<Row, EXACT>(S, d.v, d.ids, 1u, a.M, a.dim, lr, a.reuse, true, false, g, bad_src,
+                          a.fast);
   for (int c0 = kChunk; c0 < nsamp; c0 += kChunk) {  // only when n_neg >= kChunk
     int32_t ids[kChunk];
 #pragma unroll
