@@ -127,24 +127,34 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
     const int64_t items = sources ? n_sources : num_vertices;
     int rc = grid_for((const void *)var.pass, var.G, max_groups, items, &grid);
     if (rc) return rc;
-    // a launch capped below full occupancy is latency-bound: use the
-    // prefetching variant (GB_PIPE=0/1 forces the choice for experiments)
+    // A launch whose in-flight cap is below what the throughput variant holds
+    // on the GPU is latency-bound (small levels): switch to the latency
+    // variant -- widest lane layout, batched index fetch and batched dots,
+    // one warp per block so the groups spread over all SMs -- when the cap
+    // fits its capacity.  GB_PIPE=0/1 forces the choice for experiments.
     int occ = 0;
     GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)var.pass,
                                                               kBlock, 0));
-    bool pipe = (int64_t)grid < (int64_t)num_sms() * std::max(occ, 1);
-    if (const char *env = std::getenv("GB_PIPE")) pipe = std::atoi(env) != 0;
+    const int64_t full = (int64_t)num_sms() * std::max(occ, 1) * (kBlock / var.G);
+    const int64_t groups = std::min<int64_t>(max_groups > 0 ? max_groups : INT64_MAX, items);
+    Variant lat;
+    bool pipe = false;
+    int occ1 = 0;
+    if (groups < full && pick_variant(dim, aligned16(M, dim), exact, lat, true)) {
+      GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &occ1, (const void *)lat.pass_pipe, 32, 0));
+      pipe = groups <= (int64_t)num_sms() * std::max(occ1, 1) * (32 / lat.G);
+    }
+    if (const char *env = std::getenv("GB_PIPE")) {
+      pipe = std::atoi(env) != 0 && pick_variant(dim, aligned16(M, dim), exact, lat, true);
+      if (pipe)
+        GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &occ1, (const void *)lat.pass_pipe, 32, 0));
+    }
     if (pipe) {
-      // latency-bound: widest lane layout, one warp per block so the capped
-      // groups spread over as many SMs as possible instead of sharing a few
-      GB_REQUIRE(pick_variant(dim, aligned16(M, dim), exact, var, true),
-                 "gb_train_passes: dim %d unsupported", dim);
-      fn = var.pass_pipe;
-      const int64_t gpw = 32 / var.G;
-      const int64_t groups = std::min<int64_t>(max_groups > 0 ? max_groups : INT64_MAX, items);
+      fn = lat.pass_pipe;
+      const int64_t gpw = 32 / lat.G;
       const int64_t warps = std::max<int64_t>(1, (groups + gpw - 1) / gpw);
-      int occ1 = 0;
-      GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, (const void *)fn, 32, 0));
       grid = (int)std::min<int64_t>(warps, (int64_t)num_sms() * std::max(occ1, 1));
       block = 32;
     }

@@ -380,55 +380,76 @@ struct PassArgs {
   int64_t *status;
 };
 
-// Index half of a source (read-only data: xadj, adj, the RNG) -- prefetched
-// one source ahead so the xadj -> adj -> positive-id chain overlaps the
-// previous source's row updates.  Prefetching it does not change results.
+// Index half of a source: v, the positive (xadj -> adj), the first chunk of
+// negatives, the RNG key and the pass's lr.  Read-only inputs, so computing
+// it early never changes results.
 struct SourceIdx {
-  int64_t v;
-  int64_t x0;
-  int64_t deg;
+  int32_t v;
+  int32_t ids[kChunk];  // positive + up to kChunk-1 negatives
   uint64_t key;
-  int32_t ids[kChunk];  // first chunk: positive + up to kChunk-1 negatives
+  float lr;
+  int32_t epoch;
   bool active;
 };
 
 __device__ __forceinline__ void fetch_source(const PassArgs &a, int64_t p, int64_t i, bool ok,
                                              SourceIdx &d) {
   d.active = ok;
+  d.v = 0;
+  d.key = 0;
+  d.lr = 0.0f;
+  d.epoch = 0;
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) d.ids[j] = -1;
   if (!ok) return;
-  d.v = a.sources ? (int64_t)__ldg(a.sources + i) : i;
-  d.x0 = __ldg(a.xadj + d.v);
-  d.deg = __ldg(a.xadj + d.v + 1) - d.x0;
-  if (d.deg == 0) {  // isolated sources are skipped (trainer.py:198-200)
+  const int64_t v = a.sources ? (int64_t)__ldg(a.sources + i) : i;
+  const int64_t x0 = __ldg(a.xadj + v);
+  const int64_t deg = __ldg(a.xadj + v + 1) - x0;
+  if (deg == 0) {  // isolated sources are skipped (trainer.py:198-200)
     d.active = false;
     return;
   }
-  d.key = stream_key(a.seed, a.stream, (uint64_t)p, (uint64_t)d.v);
+  d.v = (int32_t)v;
+  d.key = stream_key(a.seed, a.stream, (uint64_t)p, (uint64_t)v);
+  d.epoch = (int32_t)(p / a.ppe);
+  d.lr = __ldg(a.lr + d.epoch);
   const int nsamp = 1 + a.n_neg;
 #pragma unroll
   for (int j = 0; j < kChunk; ++j) {
     if (j >= nsamp)
       d.ids[j] = -1;
     else if (j == 0)  // positive: uniform neighbour (trainer.py:203)
-      d.ids[j] = __ldg(a.adj + d.x0 + draw_below(d.key, 0, d.deg));
+      d.ids[j] = __ldg(a.adj + x0 + draw_below(d.key, 0, deg));
     else  // negatives: uniform over V (trainer.py:205-206)
       d.ids[j] = (int32_t)draw_below(d.key, (uint64_t)j, a.V);
   }
 }
 
-// Processes one source whose index half is in `d` (run_chunk per chunk).
-template <class Row, bool EXACT>
+// Lane k's SourceIdx, broadcast to its whole group.
+__device__ __forceinline__ SourceIdx shfl_source(const SourceIdx &d, int k, unsigned gmask,
+                                                 int G) {
+  SourceIdx o;
+  o.active = __shfl_sync(gmask, (int)d.active, k, G) != 0;
+  o.v = __shfl_sync(gmask, d.v, k, G);
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) o.ids[j] = __shfl_sync(gmask, d.ids[j], k, G);
+  o.key = __shfl_sync(gmask, d.key, k, G);
+  o.lr = __shfl_sync(gmask, d.lr, k, G);
+  o.epoch = __shfl_sync(gmask, d.epoch, k, G);
+  return o;
+}
+
+// Row half of a source: gather, chained updates, write-back.
+template <class Row, bool EXACT, bool BATCH>
 __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &g,
-                                             const SourceIdx &d, int64_t p, bool &bad,
-                                             int64_t &first_bad) {
+                                             const SourceIdx &d, bool &bad, int &first_bad) {
   const int nsamp = 1 + a.n_neg;
-  const int64_t epoch = p / a.ppe;
-  const double lr = (double)__ldg(a.lr + epoch);
+  const double lr = (double)d.lr;
   Row S;
-  S.load(a.M + d.v * (int64_t)a.dim, g.gl, a.dim);
+  S.load(a.M + (int64_t)d.v * a.dim, g.gl, a.dim);
   bool bad_src = false;
-  if (EXACT || !batched_chunk<Row>(S, d.v, d.ids, 1u, a.M, a.dim, lr, a.reuse, g, bad_src,
-                                   a.fast))
+  if (EXACT || !BATCH ||
+      !batched_chunk<Row>(S, d.v, d.ids, 1u, a.M, a.dim, lr, a.reuse, g, bad_src, a.fast))
     run_chunk<Row, EXACT>(S, d.v, d.ids, 1u, a.M, a.dim, lr, a.reuse, true, false, g, bad_src,
                           a.fast);
   for (int c0 = kChunk; c0 < nsamp; c0 += kChunk) {  // only when n_neg >= kChunk
@@ -439,31 +460,41 @@ __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &
     run_chunk<Row, EXACT>(S, d.v, ids, 0u, a.M, a.dim, lr, a.reuse, true, false, g, bad_src,
                           a.fast);
   }
-  S.store(a.M + d.v * (int64_t)a.dim, g.gl, a.dim);
+  S.store(a.M + (int64_t)d.v * a.dim, g.gl, a.dim);
   if (bad_src) {
     bad = true;
-    first_bad = min(first_bad, epoch);
+    first_bad = min(first_bad, d.epoch);
   }
 }
 
-// PIPE = false: throughput variant for full-occupancy (HBM-bound) launches.
-// PIPE = true: latency variant for capped launches on small levels -- the
-// index half of the next source is fetched before the current source's row
-// updates (more registers, one block per SM is plenty there).
-template <class Row, bool EXACT, bool PIPE>
-__global__ void __launch_bounds__(kBlock, PIPE ? 1 : Row::kMinBlocks)
+// Each group walks a sequence of steps s = 0, 1, ...: step s is pass
+// pass_begin + s / spp, item warp_base + (s % spp)*eff + (its slot), with spp
+// (steps per pass) uniform across the warp so its groups stay in lockstep.
+// Indices come in batches: lane l of a group fetches step s0 + l, then the
+// group trains the G sources one by one from shuffled indices -- the
+// sources -> xadj -> key -> adj chain and the RNG run once per G sources,
+// G-way parallel, instead of redundantly on every lane for every source.
+// BATCH = true (latency variant, capped launches): batched-dot chunks and one
+// block per SM worth of registers.
+template <class Row, bool EXACT, bool BATCH>
+__global__ void __launch_bounds__(kBlock, BATCH ? 1 : Row::kMinBlocks)
     train_passes_kernel(PassArgs a) {
+  constexpr int G = Row::G;
   const GroupCtx g = group_ctx<Row>();
   const Slots<Row> sl(a.max_groups);
   if (sl.warp_idle()) return;
   bool bad = false;
-  int64_t first_bad = INT64_MAX;
+  int first_bad = INT_MAX;
   const int64_t n = a.sources ? a.n_sources : a.V;
+  if (sl.warp_base >= n) return;
   const int64_t lane_off = sl.gid - sl.warp_base;
-  if constexpr (!PIPE) {
+  if constexpr (!BATCH) {
+    // throughput variant (full occupancy, HBM-bound): the index chain is
+    // computed inline per source -- its latency hides behind other warps and
+    // this keeps the kernel within 128 registers (2 blocks per SM)
     const int nsamp = 1 + a.n_neg;
     for (int64_t p = a.pass_begin; p < a.pass_begin + a.n_passes; ++p) {
-      const int64_t epoch = p / a.ppe;
+      const int epoch = (int)(p / a.ppe);
       const double lr = (double)__ldg(a.lr + epoch);
       for (int64_t base = sl.warp_base; base < n; base += sl.eff) {
         const int64_t i = base + lane_off;
@@ -499,26 +530,21 @@ __global__ void __launch_bounds__(kBlock, PIPE ? 1 : Row::kMinBlocks)
       }
     }
   } else {
-    // (pass, item) cursor: the warp-uniform `base` advances by eff per step
-    // and wraps into the next pass.
-    const int64_t p_end = a.pass_begin + a.n_passes;
-    int64_t p = a.pass_begin, base = sl.warp_base;
-    if (base >= n) return;
-    SourceIdx cur;
-    fetch_source(a, p, base + lane_off, sl.enabled && base + lane_off < n, cur);
-    while (p < p_end) {
-      int64_t np = p, nbase = base + sl.eff;
-      if (nbase >= n) {
-        ++np;
-        nbase = sl.warp_base;
+    const int64_t spp = (n - sl.warp_base + sl.eff - 1) / sl.eff;
+    const int64_t total = spp * a.n_passes;
+    for (int64_t s0 = 0; s0 < total; s0 += G) {
+      SourceIdx mine;
+      {
+        const int64_t s = s0 + g.gl;
+        const int64_t q = s / spp;
+        const int64_t i = sl.warp_base + (s - q * spp) * sl.eff + lane_off;
+        fetch_source(a, a.pass_begin + q, i, s < total && sl.enabled && i < n, mine);
       }
-      SourceIdx nxt;
-      fetch_source(a, np, nbase + lane_off, np < p_end && sl.enabled && nbase + lane_off < n,
-                   nxt);
-      if (cur.active) train_source<Row, EXACT>(a, g, cur, p, bad, first_bad);
-      cur = nxt;
-      p = np;
-      base = nbase;
+      const int kmax = (int)(total - s0 < G ? total - s0 : G);
+      for (int k = 0; k < kmax; ++k) {
+        const SourceIdx d = shfl_source(mine, k, g.gmask, G);
+        if (d.active) train_source<Row, EXACT, BATCH>(a, g, d, bad, first_bad);
+      }
     }
   }
   if (bad && g.gl == 0) {
