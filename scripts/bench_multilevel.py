@@ -30,7 +30,8 @@ t_graph = time.perf_counter() - t0
 print(json.dumps({"graph": which, "vertices": g.num_vertices, "arcs": g.num_edges,
                   "undirected_edges": g.num_edges // 2, "build_s": t_graph}), flush=True)
 cfg = gb.TrainConfig(dim=dim, total_epochs=epochs, smoothing_ratio=0.3, learning_rate=0.035,
-                     negative_samples=3, seed=1, epoch_unit="edge-scaled",
+                     negative_samples=3, seed=1,
+                     epoch_unit=os.environ.get("UNIT", "edge-scaled"),
                      max_inflight=int(os.environ.get("CAP", "0")))
 t0 = time.perf_counter()
 h = gb.coarsen_all(g, threshold=100)

@@ -1,0 +1,189 @@
+"""Sharded part-pair training (paper_2008_12336_b200/tournament.py).
+
+CPU: the circle-method schedule covers rotation_pairs(K) once per rotation
+with disjoint pairs per round and neighbour-only moves; the schedule +
+exchange run over gloo with world_size 2 and 3 (the pair step replaced by
+the oracle's C restatement of bigtrain.py's pool/pair kernels) equals the
+sequential execution of the same pair order.  GPU: the device pair kernel
+(deterministic) under virtual ranks equals that sequential oracle replay
+bit for bit.
+"""
+from __future__ import annotations
+
+import os
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2008_12336_b200 as gb
+from paper_2008_12336_b200 import tournament as tn
+from paper_2008_12336_b200.graph import Graph
+
+
+# -- schedule ----------------------------------------------------------------------
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
+def test_rounds_cover_every_pair_once_disjointly(G):
+    K = 2 * G
+    rounds = tn.tournament_rounds(K)
+    assert len(rounds) == K
+    seen = [pr for rnd in rounds for pr in rnd]
+    assert sorted(seen) == sorted(gb.rotation_pairs(K))
+    for rnd in rounds:
+        parts = [p for pr in rnd for p in set(pr)]
+        assert len(parts) == len(set(parts)) == K
+
+
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
+def test_shift_moves_are_neighbour_only_and_a_permutation(G):
+    K = 2 * G
+    moves = tn.shift_moves(K)
+    for sr, ss, dr, ds in moves:
+        assert abs(sr - dr) <= 1
+    per_rank_send = [sum(1 for m in moves if m[0] == r and m[2] != r) for r in range(G)]
+    assert max(per_rank_send) <= 2
+    # applying the moves to holdings equals shifting the arrangement
+    arr = tn.initial_arrangement(K)
+    hold = [list(h) for h in tn.holdings(arr)]
+    new = [list(h) for h in hold]
+    for sr, ss, dr, ds in moves:
+        new[dr][ds] = hold[sr][ss]
+    assert [tuple(h) for h in new] == tn.holdings(tn.shift(arr))
+    for _ in range(K - 1):
+        arr = tn.shift(arr)
+    assert arr == tn.initial_arrangement(K)
+
+
+def test_rejects_odd_part_count():
+    with pytest.raises(gb.ConfigError):
+        tn.tournament_rounds(3)
+
+
+# -- CPU pair step (the oracle, as the checker) -----------------------------------
+def _graph(orc, scale=9, samples=3000, seed=5):
+    x, a = orc.rmat_graph(scale, samples, seed, densify_ids=True)
+    return Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a), x, a
+
+
+def _oracle_pair_fn(orc, x, a, B, n_s):
+    def fn(Ma, Mb, s):
+        A = Ma.numpy()
+        Bm = A if s.a == s.b else Mb.numpy()
+        tj = orc.fill_pool_side(x, a, s.lo_a, s.hi_a, s.lo_b, s.hi_b, B, s.seed, 0)
+        orc.train_pool_side(A, Bm, tj, s.lo_b, s.hi_b - s.lo_b, n_s, s.lr, s.seed, 2)
+        if s.a != s.b:
+            tk = orc.fill_pool_side(x, a, s.lo_b, s.hi_b, s.lo_a, s.hi_a, B, s.seed, 1)
+            orc.train_pool_side(Bm, A, tk, s.lo_a, s.hi_a - s.lo_a, n_s, s.lr, s.seed, 3)
+    return fn
+
+
+def _sequential_replay(orc, g, x, a, M, cfg, e_i, G, B=5, stream=0):
+    """The same pair order on one full matrix, no parts, no exchange."""
+    K = 2 * G
+    V = M.shape[0]
+    bnd = (np.arange(K + 1, dtype=np.int64) * V) // K
+    rot = tn.tournament_rotations(g, cfg, e_i, K, B)
+    idx = tn.pair_index(K)
+    P = len(idx)
+    for r, (pa, pb) in tn.sequential_order(K, rot):
+        lr = gb.lr_at(cfg.learning_rate, r, rot)
+        seed = gb.bigtrain._derived_seed(cfg.seed, stream, r * P + idx[(pa, pb)])
+        la, ha, lb, hb = int(bnd[pa]), int(bnd[pa + 1]), int(bnd[pb]), int(bnd[pb + 1])
+        A = M[la:ha]
+        Bm = A if pa == pb else M[lb:hb]
+        tj = orc.fill_pool_side(x, a, la, ha, lb, hb, B, seed, 0)
+        A2 = np.ascontiguousarray(A)
+        B2 = A2 if pa == pb else np.ascontiguousarray(Bm)
+        orc.train_pool_side(A2, B2, tj, lb, hb - lb, cfg.negative_samples, lr, seed, 2)
+        if pa != pb:
+            tk = orc.fill_pool_side(x, a, lb, hb, la, ha, B, seed, 1)
+            orc.train_pool_side(B2, A2, tk, la, ha - la, cfg.negative_samples, lr, seed, 3)
+        M[la:ha] = A2
+        if pa != pb:
+            M[lb:hb] = B2
+    return rot
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 4])
+def test_virtual_ranks_equal_sequential_replay(orc, G):
+    g, x, a = _graph(orc)
+    cfg = gb.TrainConfig(dim=16, negative_samples=3, seed=3, deterministic=True)
+    M0 = orc.init_embedding(g.num_vertices, 16, 1)
+    ref = M0.copy()
+    rot = _sequential_replay(orc, g, x, a, ref, cfg, 30, G)
+    M = torch.from_numpy(M0.copy())
+    st = tn.train_tournament(g, M, cfg, 30, num_ranks=G,
+                             pair_fn=_oracle_pair_fn(orc, x, a, 5, 3))
+    assert st["rotations"] == rot and st["K"] == 2 * G
+    assert st["pairs"] == rot * (2 * G) * (2 * G + 1) // 2
+    assert np.array_equal(M.numpy(), ref)
+    assert not np.array_equal(ref, M0)
+
+
+def _gloo_worker(rank, world, port, out_path):
+    import torch.distributed as dist
+    from oracle import oracle as orc
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g, x, a = _graph(orc)
+        cfg = gb.TrainConfig(dim=16, negative_samples=3, seed=3, deterministic=True)
+        M = torch.from_numpy(orc.init_embedding(g.num_vertices, 16, 1))
+        st = tn.train_tournament(g, M, cfg, 30, pair_fn=_oracle_pair_fn(orc, x, a, 5, 3))
+        np.save(f"{out_path}.{rank}.npy", M.numpy())
+        np.save(f"{out_path}.{rank}.stats.npy",
+                np.array([st["pairs"], st["exchange_bytes"], st["ranks"]]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_tournament_equals_sequential_replay(orc, world):
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "m")
+        mp.spawn(_gloo_worker, args=(world, port, out), nprocs=world, join=True)
+        g, x, a = _graph(orc)
+        cfg = gb.TrainConfig(dim=16, negative_samples=3, seed=3, deterministic=True)
+        ref = orc.init_embedding(g.num_vertices, 16, 1)
+        rot = _sequential_replay(orc, g, x, a, ref, cfg, 30, world)
+        K = 2 * world
+        for r in range(world):
+            M = np.load(f"{out}.{r}.npy")
+            assert np.array_equal(M, ref), f"rank {r}"
+            pairs, sent, ranks = np.load(f"{out}.{r}.stats.npy").tolist()
+            assert ranks == world and pairs == rot * K * (K + 1) // 2
+            # every rank sends <= 2 parts per shift; K-1 shifts per rotation
+            max_rows = -(-g.num_vertices // K)
+            assert 0 < sent <= rot * (K - 1) * world * 2 * max_rows * 16 * 4
+
+
+# -- GPU: device pair kernel under the tournament ----------------------------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("G", [1, 2, 4])
+def test_device_tournament_deterministic_bit_exact(cuda, orc, G):
+    g, x, a = _graph(orc, scale=10, samples=6000)
+    cfg = gb.TrainConfig(dim=32, negative_samples=3, seed=4, deterministic=True)
+    M0 = orc.init_embedding(g.num_vertices, 32, 2)
+    ref = M0.copy()
+    _sequential_replay(orc, g, x, a, ref, cfg, 20, G)
+    M = torch.from_numpy(M0.copy()).cuda()
+    tn.train_tournament(g, M, cfg, 20, num_ranks=G)
+    assert np.array_equal(M.cpu().numpy(), ref)
+
+
+@pytest.mark.gpu
+def test_device_tournament_hogwild_counts(cuda, orc):
+    g, x, a = _graph(orc, scale=12, samples=40000)
+    cfg = gb.TrainConfig(dim=128, negative_samples=3, seed=4, epoch_unit="edge-scaled")
+    M = torch.from_numpy(orc.init_embedding(g.num_vertices, 128, 2)).cuda()
+    st = tn.train_tournament(g, M, cfg, 2, num_ranks=4)
+    assert st["pos_updates"] > 0 and st["neg_updates"] == 3 * st["pos_updates"]
+    assert bool(torch.isfinite(M).all())
