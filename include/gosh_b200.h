@@ -197,6 +197,32 @@ int gb_train_pool_side(float *Msrc, float *Mtgt, int dim,
                        unsigned flags, int64_t max_groups, int64_t *status,
                        void *stream_handle);
 
+/* ---- L4: link-prediction evaluator (evaluate.py), SURVEY.md 8(f) rank 1 ----
+ * hadamard_features (evaluate.py:69-78): X[i*dim+t] = fl32(M[u_i,t]*M[v_i,t])
+ * for pairs[2i]=u_i, pairs[2i+1]=v_i. */
+int gb_hadamard_features(const float *M, int64_t num_rows, int dim,
+                         const int64_t *pairs, int64_t n, float *X,
+                         void *stream_handle);
+
+/* One epoch of train_logreg's mini-batch descent (evaluate.py:128-140) over
+ * the permutation perm[n] (numpy's rng.permutation, drawn on the host):
+ * batches of batch_size rows in perm order, w (dim doubles) and *b updated
+ * in place in device memory. */
+int gb_logreg_epoch(const float *X, int dim, const int8_t *labels,
+                    const int64_t *perm, int64_t n, int batch_size,
+                    double step, double *w, double *b, void *stream_handle);
+
+/* predict_scores (evaluate.py:146-147): out[i] = X[i] . w + b (fp64). */
+int gb_predict_scores(const float *X, int dim, int64_t n, const double *w,
+                      double b, double *out, void *stream_handle);
+
+/* auc_roc (evaluate.py:150-167): *rank2_pos (device) = sum over positives
+ * of doubled midranks; AUC = (r2p - P(P+1)) / (2 P N) on the host. */
+int gb_auc_roc_workspace(int64_t n, size_t *bytes);
+int gb_auc_roc(const double *scores, const int8_t *labels, int64_t n,
+               unsigned long long *rank2_pos, void *workspace,
+               size_t workspace_bytes, void *stream_handle);
+
 #ifdef __cplusplus
 }
 #endif

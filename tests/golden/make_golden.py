@@ -306,12 +306,50 @@ def make_rmat():
     save("rmat.npz", **out)
 
 
+def make_eval():
+    # evaluate.py: midrank AUCROC with heavy ties, and train_logreg +
+    # predict_scores on Hadamard features of a fixed embedding
+    from mlembed import evaluate as rev
+    out = {}
+    rng = np.random.default_rng(11)
+    for k, (n, levels) in enumerate(((50, 4), (2000, 37), (5000, 100000), (777, 1))):
+        s = np.round(rng.normal(size=n) * levels) / levels
+        y = (rng.random(n) < 0.4).astype(np.int8)
+        y[0], y[1] = 1, 0
+        out[f"a{k}_scores"] = s
+        out[f"a{k}_labels"] = y
+        out[f"a{k}_auc"] = np.float64(rev.auc_roc(s, y))
+    g = synth.chung_lu_graph(400, 1600, 2.5, seed=9)
+    M = trainer.init_embedding(g.num_vertices, 16, 3) * 40.0
+    pos = g.undirected_pairs()
+    neg = rev.sample_negative_edges(g, pos.shape[0], seed=5)
+    pairs = np.vstack([pos, neg])
+    labels = np.concatenate([np.ones(len(pos), np.int8), np.zeros(len(neg), np.int8)])
+    f = rev.hadamard_features(M, pairs, labels)
+    out["M"] = M
+    out["pairs"] = pairs
+    out["labels"] = labels
+    out["rows"] = f.rows
+    out["neg"] = neg
+    for k, hyper in enumerate((rev.LogRegConfig(epochs=20, seed=4),
+                               rev.LogRegConfig(epochs=3, batch_size=100, step=0.5, seed=2),
+                               rev.LogRegConfig(seed=1, single_pass=True))):
+        model = rev.train_logreg(f, hyper)
+        sc = rev.predict_scores(model, f.rows)
+        out[f"l{k}_hyper"] = np.asarray([hyper.epochs, hyper.batch_size, hyper.seed,
+                                         int(hyper.single_pass)], dtype=np.int64)
+        out[f"l{k}_step"] = np.float64(hyper.step)
+        out[f"l{k}_w"] = model.weights
+        out[f"l{k}_b"] = np.float64(model.bias)
+        out[f"l{k}_scores"] = sc
+        out[f"l{k}_auc"] = np.float64(rev.auc_roc(sc, labels))
+    save("eval.npz", **out)
+
+
+GENERATORS = {"rng": make_rng, "update": make_update, "train_pass": make_train_pass,
+              "coarsen": make_coarsen, "csr": make_csr, "pool": make_pool,
+              "large": make_large_and_multilevel, "rmat": make_rmat, "eval": make_eval}
+
 if __name__ == "__main__":
-    make_rng()
-    make_update()
-    make_train_pass()
-    make_coarsen()
-    make_csr()
-    make_pool()
-    make_large_and_multilevel()
-    make_rmat()
+    for name in (sys.argv[1:] or GENERATORS):
+        GENERATORS[name]()
