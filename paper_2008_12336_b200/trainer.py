@@ -19,6 +19,7 @@ knobs extend TrainConfig:
 """
 from __future__ import annotations
 
+import os
 import struct
 from dataclasses import dataclass
 from typing import IO, NamedTuple
@@ -36,6 +37,10 @@ EMBED_VERSION = 1
 SIGMOID_CLAMP = 10.0
 LR_FLOOR = 1e-4
 EPOCH_UNITS = ("vertex-pass", "edge-scaled")
+# auto in-flight policy max(FLOOR, V / DIVISOR); the environment overrides
+# exist for staleness/quality experiments (scripts/auc_modes.py)
+INFLIGHT_FLOOR = int(os.environ.get("GB_INFLIGHT_FLOOR", "64"))
+INFLIGHT_DIVISOR = int(os.environ.get("GB_INFLIGHT_DIV", "64"))
 
 
 @dataclass
@@ -93,7 +98,7 @@ def inflight_cap(cfg: TrainConfig, num_vertices: int) -> int:
         return 1
     if cfg.max_inflight > 0:
         return cfg.max_inflight
-    return max(64, num_vertices // 64)
+    return max(INFLIGHT_FLOOR, num_vertices // INFLIGHT_DIVISOR)
 
 
 def init_embedding(num_rows: int, dim: int, seed: int) -> np.ndarray:

@@ -3,6 +3,12 @@ one GPU: coarsening ladder + per-level training time (GPU box).
 
     python scripts/bench_multilevel.py [c3|c1] [epochs]
 
+CPU=1 adds the reference's CPU path timed on this box's host cores (the
+oracle's C restatement: sequential coarsen_all = the reference's parity
+path, then train_level per level with all host threads).  Levels whose CPU
+training would exceed CPU_LEVEL_S seconds are timed on a bounded number of
+passes and extrapolated at the measured rate (reported as such).
+
 Mirrors train_multilevel (trainer.py:252-288) step by step so each level can
 be timed; prints one JSON line per level and a summary line."""
 import json
@@ -62,3 +68,50 @@ torch.cuda.synchronize()
 print(json.dumps({"summary": which, "embed_s": t_coarsen + t_train, "coarsen_s": t_coarsen,
                   "train_s": t_train, "updates": total_upd,
                   "upd_per_s": total_upd / t_train}), flush=True)
+
+if os.environ.get("CPU") == "1":
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as orc
+    threads = orc.max_threads()
+    budget_s = float(os.environ.get("CPU_LEVEL_S", "20"))
+    x0, a0 = g.device_csr()
+    x0 = x0.cpu().numpy()
+    a0 = a0[: g.num_edges].cpu().numpy()
+    t0 = time.perf_counter()
+    graphs, maps, stalled = orc.coarsen_all(x0, a0, 100)
+    cpu_coarsen = time.perf_counter() - t0
+    assert [len(x) - 1 for x, _ in graphs] == [x.num_vertices for x in h.graphs]
+    cpu_train, cpu_upd = 0.0, 0
+    Mc = orc.init_embedding(len(graphs[-1][0]) - 1, dim, cfg.seed)
+    for i in range(len(graphs) - 1, -1, -1):
+        x, a = graphs[i]
+        V, E = len(x) - 1, int(x[-1])
+        ppe = orc.passes_per_epoch(V, E, cfg.epoch_unit)
+        e_i = int(plan[i])
+        non_iso = int((np.diff(x) > 0).sum())
+        passes_total = e_i * ppe
+        # calibrate: one pass, then as many as fit the level budget
+        t0 = time.perf_counter()
+        orc.train_pass(x, a, Mc, cfg.learning_rate, 3, cfg.seed, i, 0, nthreads=threads)
+        one = max(time.perf_counter() - t0, 1e-6)
+        n_run = int(min(passes_total, max(1, budget_s / one)))
+        t0 = time.perf_counter()
+        for p in range(1, n_run):
+            orc.train_pass(x, a, Mc, cfg.learning_rate, 3, cfg.seed, i, p, nthreads=threads)
+        el = one + time.perf_counter() - t0
+        rate = n_run * non_iso * 4 / el
+        upd = passes_total * non_iso * 4
+        est = upd / rate
+        cpu_train += est
+        cpu_upd += upd
+        print(json.dumps({"cpu_level": i, "V": V, "passes": passes_total, "passes_timed": n_run,
+                          "upd_per_s": rate, "s_est": est, "threads": threads}), flush=True)
+        if i > 0:
+            Mc = orc.expand(Mc, maps[i - 1][0])
+    print(json.dumps({"cpu_summary": which, "threads": threads, "coarsen_s": cpu_coarsen,
+                      "train_s_est": cpu_train, "embed_s_est": cpu_coarsen + cpu_train,
+                      "updates": cpu_upd, "kind": "port (oracle/gosh_oracle.c)",
+                      "gpu_embed_s": t_coarsen + t_train,
+                      "speedup_est": (cpu_coarsen + cpu_train) / (t_coarsen + t_train)}),
+          flush=True)
+
