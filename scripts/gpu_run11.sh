@@ -4,3 +4,4 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:trai
 for div in 64 16 4 1; do
 GB_INFLIGHT_DIV=$div GRAPH=c1 MODES=cap0 SEEDS=1,2,3,4,5 timeout 900 python scripts/auc_modes.py > gpurun_out/auc_c1_div$div.jsonl 2> gpurun_out/auc_c1_div$div.err; tail -2 gpurun_out/auc_c1_div$div.err; cat gpurun_out/auc_c1_div$div.jsonl
 done
+GRAPH=c3 MODES=cap0,cap4096,cap1024,cap256 SEEDS=1,2 UNIT=vertex-pass EPOCHS=100 EVAL_SAMPLE=1000000 timeout 1500 python scripts/auc_modes.py > gpurun_out/auc_c3_caps.jsonl 2> gpurun_out/auc_c3_caps.err; tail -3 gpurun_out/auc_c3_caps.err; cat gpurun_out/auc_c3_caps.jsonl
