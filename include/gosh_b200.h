@@ -39,6 +39,7 @@ extern "C" {
 #define GB_TRAIN_REUSE 1u  /* TrainConfig.reuse_updated_source (trainer.py:47-50) */
 #define GB_TRAIN_EXACT 2u  /* one source group, reference order, serial fp64 dot  */
 #define GB_TRAIN_FAST_SIGMOID 4u /* non-exact: fp32 cancellation-free sigmoid     */
+#define GB_TRAIN_ATOMIC 8u /* non-exact: sample rows written back by vector reductions (no lost updates) */
 
 /* csr build flags */
 #define GB_CSR_DROP_SELF 1u  /* from_edges drops self-loops (graph.py:127-128)  */

@@ -23,6 +23,7 @@ GB_E_INVALID = -1
 GB_TRAIN_REUSE = 1
 GB_TRAIN_EXACT = 2
 GB_TRAIN_FAST_SIGMOID = 4
+GB_TRAIN_ATOMIC = 8
 GB_CSR_DROP_SELF = 1
 GB_CSR_SYMMETRIZE = 2
 STATUS_WORDS = 4

@@ -120,7 +120,7 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
   GB_REQUIRE(!sources || n_sources >= 0, "gb_train_passes: bad source list");
   PassArgs a{num_vertices, xadj, adj, sources, n_sources, M, dim, n_neg, seed, rng_stream, pass_begin, n_passes,
              passes_per_epoch, lr_per_epoch, (flags & GB_TRAIN_REUSE) != 0,
-             (flags & GB_TRAIN_FAST_SIGMOID) != 0, exact ? 1 : max_groups, status};
+             (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status};
   int grid = 1, block = kBlock;
   PassFn fn = var.pass;
   if (!exact) {
@@ -183,7 +183,7 @@ GB_API int gb_train_pool_side(float *Msrc, float *Mtgt, int dim, const int32_t *
              "gb_train_pool_side: dim %d unsupported", dim);
   PoolArgs a{Msrc, Mtgt, dim, targets, n_src, B, lo_t, n_t, n_neg, lr, seed, side, xadj, adj,
              lo_s, pool_side, (flags & GB_TRAIN_REUSE) != 0,
-             (flags & GB_TRAIN_FAST_SIGMOID) != 0, exact ? 1 : max_groups, status};
+             (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status};
   int grid = 1;
   if (!exact) {
     int rc = grid_for((const void *)var.pool, var.G, max_groups, n_src, &grid);
@@ -218,7 +218,7 @@ GB_API int gb_apply_sample_lists(float *M, int dim, int64_t n_src, const int64_t
   GB_REQUIRE(pick_variant(dim, aligned16(M, dim), exact, var),
              "gb_apply_sample_lists: dim %d unsupported", dim);
   ListArgs a{M, dim, n_src, src, k, samples, labels, lr, (flags & GB_TRAIN_REUSE) != 0,
-             (flags & GB_TRAIN_FAST_SIGMOID) != 0, exact ? 1 : max_groups, status};
+             (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status};
   int grid = 1;
   if (!exact) {
     int rc = grid_for((const void *)var.lists, var.G, max_groups, n_src, &grid);

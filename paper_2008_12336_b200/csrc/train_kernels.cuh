@@ -64,6 +64,18 @@ struct VecRow {
       __stcg(reinterpret_cast<float4 *>(row) + k * G + gl, v);
     }
   }
+  // Hogwild write-back of increments: elements 4k0/4..+3 (one float4) by a
+  // 16-byte vector reduction (red.global.add.v4.f32, performed at L2), so
+  // concurrent updates of the same row are all applied instead of the last
+  // store winning.  Like every f32 global reduction it flushes subnormals.
+  static constexpr int kRedWidth = 4;
+  __device__ __forceinline__ static void red_part(float *row, int gl, int, int k0,
+                                                  const float (&d)[4]) {
+    float *p = row + 4 * ((k0 / 4) * G + gl);
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(d[0]),
+                 "f"(d[1]), "f"(d[2]), "f"(d[3])
+                 : "memory");
+  }
   // Serial dot in ascending element order (the reference's loop order,
   // trainer.py:122-123): element t = 4*(k*G + l) + c.
   __device__ __forceinline__ static double serial_dot(const VecRow &a, const VecRow &b,
@@ -101,6 +113,11 @@ struct ScalarRow {
 #pragma unroll
     for (int k = 0; k < NS; ++k)
       if (valid(k, gl, dim)) __stcg(row + k * 32 + gl, x[k]);
+  }
+  static constexpr int kRedWidth = 1;
+  __device__ __forceinline__ static void red_part(float *row, int gl, int dim, int k,
+                                                  const float (&d)[1]) {
+    if (valid(k, gl, dim)) atomicAdd(row + k * 32 + gl, d[0]);
   }
   __device__ __forceinline__ static double serial_dot(const ScalarRow &a, const ScalarRow &b,
                                                       unsigned gmask, int gl, int dim) {
@@ -181,6 +198,41 @@ __device__ __forceinline__ void update_pair(Row &S, Row &R, float sc, bool reuse
   }
 }
 
+// Update of a distinct sample row followed by its write-back.  atomic:
+// the row's increments fl(vo*sc) (fl(S'*sc) with reuse) are added with
+// vector reductions instead of storing the updated row -- identical values
+// when nobody else touched the row, and no lost updates when somebody did
+// (the reference's per-element read-modify-write, trainer.py:131-140, has a
+// window of one element; a stored GPU row has one of a whole chunk).
+template <class Row>
+__device__ __forceinline__ void update_pair_writeback(Row &S, Row &R, float sc, bool reuse,
+                                                      bool atomic, float *row, int gl,
+                                                      int dim) {
+  if (!atomic) {
+    update_pair(S, R, sc, reuse);
+    R.store(row, gl, dim);
+    return;
+  }
+  constexpr int W = Row::kRedWidth;
+  if (reuse) {
+#pragma unroll
+    for (int k = 0; k < Row::E; ++k) S.x[k] = __fadd_rn(S.x[k], __fmul_rn(R.x[k], sc));
+  }
+#pragma unroll
+  for (int k0 = 0; k0 < Row::E; k0 += W) {
+    float d[W];
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      const int k = k0 + c;
+      const float vo = S.x[k];
+      if (!reuse) S.x[k] = __fadd_rn(vo, __fmul_rn(R.x[k], sc));
+      d[c] = __fmul_rn(vo, sc);  // with reuse vo is already the updated S
+      R.x[k] = __fadd_rn(R.x[k], d[c]);
+    }
+    Row::red_part(row, gl, dim, k0, d);
+  }
+}
+
 // Self-sample (s == v).  In-place rule of the single-array kernel
 // (_train_pass passes M twice): M[v] = fl(fl(vo + vo*sc) + vo*sc).  Load-once
 // rule of the two-array pool kernel on a diagonal pair (numba marks the two
@@ -230,7 +282,7 @@ __device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t
                                           unsigned pos_mask, float *__restrict__ Mtgt, int dim,
                                           double lr, bool reuse, bool self_possible,
                                           bool load_once, const GroupCtx &g, bool &bad,
-                                          bool fast = false) {
+                                          bool fast = false, bool atomic = false) {
   Row R[kChunk];
 #pragma unroll
   for (int j = 0; j < kChunk; ++j)
@@ -249,11 +301,11 @@ __device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t
     }
     double acc = row_dot<Row, EXACT>(S, R[j], g.gmask, g.gl, dim);
     float sc = nce_score(acc, b, lr, bad, fast && !EXACT);
-    update_pair(S, R[j], sc, reuse);
+    update_pair_writeback(S, R[j], sc, reuse, atomic && !EXACT, Mtgt + (int64_t)s * dim, g.gl,
+                          dim);
 #pragma unroll
     for (int jj = j + 1; jj < kChunk; ++jj)
       if (ids[jj] == s) R[jj] = R[j];
-    R[j].store(Mtgt + (int64_t)s * dim, g.gl, dim);
   }
 }
 
@@ -272,7 +324,7 @@ template <class Row>
 __device__ __forceinline__ bool batched_chunk(Row &S, int64_t src_row, const int32_t (&ids)[kChunk],
                                               unsigned pos_mask, float *__restrict__ Mtgt,
                                               int dim, double lr, bool reuse, const GroupCtx &g,
-                                              bool &bad, bool fast) {
+                                              bool &bad, bool fast, bool atomic = false) {
   static_assert(kChunk == 4, "batched_chunk assumes 4 samples");
   bool simple = true;
 #pragma unroll
@@ -328,8 +380,8 @@ __device__ __forceinline__ bool batched_chunk(Row &S, int64_t src_row, const int
 #pragma unroll
   for (int j = 0; j < kChunk; ++j) {
     if (ids[j] < 0) continue;
-    update_pair(S, R[j], sc[j], reuse);
-    R[j].store(Mtgt + (int64_t)ids[j] * dim, g.gl, dim);
+    update_pair_writeback(S, R[j], sc[j], reuse, atomic, Mtgt + (int64_t)ids[j] * dim, g.gl,
+                          dim);
   }
   return true;
 }
@@ -376,6 +428,7 @@ struct PassArgs {
   const float *__restrict__ lr;
   bool reuse;
   bool fast;
+  bool atomic;
   int64_t max_groups;
   int64_t *status;
 };
@@ -449,16 +502,17 @@ __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &
   S.load(a.M + (int64_t)d.v * a.dim, g.gl, a.dim);
   bool bad_src = false;
   if (EXACT || !BATCH ||
-      !batched_chunk<Row>(S, d.v, d.ids, 1u, a.M, a.dim, lr, a.reuse, g, bad_src, a.fast))
+      !batched_chunk<Row>(S, d.v, d.ids, 1u, a.M, a.dim, lr, a.reuse, g, bad_src, a.fast,
+                          a.atomic))
     run_chunk<Row, EXACT>(S, d.v, d.ids, 1u, a.M, a.dim, lr, a.reuse, true, false, g, bad_src,
-                          a.fast);
+                          a.fast, a.atomic);
   for (int c0 = kChunk; c0 < nsamp; c0 += kChunk) {  // only when n_neg >= kChunk
     int32_t ids[kChunk];
 #pragma unroll
     for (int j = 0; j < kChunk; ++j)
       ids[j] = c0 + j < nsamp ? (int32_t)draw_below(d.key, (uint64_t)(c0 + j), a.V) : -1;
     run_chunk<Row, EXACT>(S, d.v, ids, 0u, a.M, a.dim, lr, a.reuse, true, false, g, bad_src,
-                          a.fast);
+                          a.fast, a.atomic);
   }
   S.store(a.M + (int64_t)d.v * a.dim, g.gl, a.dim);
   if (bad_src) {
@@ -520,7 +574,7 @@ __global__ void __launch_bounds__(kBlock, BATCH ? 1 : Row::kMinBlocks)
               ids[j] = (int32_t)draw_below(key, (uint64_t)idx, a.V);
           }
           run_chunk<Row, EXACT>(S, v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, a.reuse, true,
-                                false, g, bad_src, a.fast);
+                                false, g, bad_src, a.fast, a.atomic);
         }
         S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
         if (bad_src) {
@@ -576,6 +630,7 @@ struct PoolArgs {
   uint64_t pool_side;
   bool reuse;
   bool fast;
+  bool atomic;
   int64_t max_groups;
   int64_t *status;
 };
@@ -651,7 +706,7 @@ __global__ void __launch_bounds__(kBlock, Row::kMinBlocks) train_pool_kernel(Poo
       }
       pos_count += __popc(pos_mask);
       run_chunk<Row, EXACT>(S, i, ids, pos_mask, a.Mtgt, a.dim, a.lr, a.reuse, diagonal, true,
-                            g, bad, a.fast);
+                            g, bad, a.fast, a.atomic);
     }
     if (loaded) S.store(a.Msrc + i * (int64_t)a.dim, g.gl, a.dim);
   }
@@ -680,6 +735,7 @@ struct ListArgs {
   double lr;
   bool reuse;
   bool fast;
+  bool atomic;
   int64_t max_groups;
   int64_t *status;
 };
@@ -706,7 +762,7 @@ __global__ void __launch_bounds__(kBlock, Row::kMinBlocks) apply_lists_kernel(Li
         if (idx < a.k && a.labels[idx]) pos_mask |= 1u << j;
       }
       run_chunk<Row, EXACT>(S, v, ids, pos_mask, a.M, a.dim, a.lr, a.reuse, true, false, g, bad,
-                            a.fast);
+                            a.fast, a.atomic);
     }
     S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
   }

@@ -148,7 +148,8 @@ def device_pair_fn(g: Graph, cfg: TrainConfig, B: int) -> tuple[PairFn, torch.Te
     _lib.require_cuda()
     csr = g.device_csr()
     flags = (_lib.GB_TRAIN_REUSE if cfg.reuse_updated_source else 0) | (
-        _lib.GB_TRAIN_EXACT if cfg.deterministic else _lib.GB_TRAIN_FAST_SIGMOID)
+        _lib.GB_TRAIN_EXACT if cfg.deterministic else _lib.GB_TRAIN_FAST_SIGMOID) | (
+        _lib.GB_TRAIN_ATOMIC if cfg.atomic_rows and not cfg.deterministic else 0)
     status = _lib.new_status()
     n_s = cfg.negative_samples
 

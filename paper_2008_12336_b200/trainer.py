@@ -15,7 +15,10 @@ knobs extend TrainConfig:
                  fp64 dot -- bit-equal to the reference at num_workers=1;
   max_inflight   cap on concurrently processed sources (0 = auto policy,
                  see `inflight_cap`), the knob that bounds Hogwild staleness
-                 on small coarse levels (SURVEY.md finding 11).
+                 on small coarse levels (SURVEY.md finding 11);
+  atomic_rows    write sample-row increments back with vector reductions
+                 (red.global.add.v4.f32) instead of storing the updated row,
+                 so concurrent updates of a hot row are never lost.
 """
 from __future__ import annotations
 
@@ -58,6 +61,7 @@ class TrainConfig:
     reuse_updated_source: bool = False
     deterministic: bool = False
     max_inflight: int = 0
+    atomic_rows: bool = False
 
     def validate(self) -> None:
         if self.dim < 1:
@@ -154,6 +158,8 @@ def _train_flags(cfg: TrainConfig) -> int:
     the fp32 cancellation-free sigmoid (fp64 dot kept)."""
     flags = _lib.GB_TRAIN_REUSE if cfg.reuse_updated_source else 0
     flags |= _lib.GB_TRAIN_EXACT if cfg.deterministic else _lib.GB_TRAIN_FAST_SIGMOID
+    if cfg.atomic_rows and not cfg.deterministic:
+        flags |= _lib.GB_TRAIN_ATOMIC
     return flags
 
 
@@ -190,7 +196,8 @@ def update_embedding(M, v: int, s: int, b: int, lr: float,
 
 
 def apply_sample_lists(M, sources, samples, labels, lr: float, deterministic: bool = False,
-                       reuse_updated_source: bool = False, max_inflight: int = 0) -> None:
+                       reuse_updated_source: bool = False, max_inflight: int = 0,
+                       atomic_rows: bool = False) -> None:
     """Fixed sample lists: source sources[i] is updated against samples[i, j]
     (j ascending; -1 skips) with label labels[j].  Sources run concurrently
     unless deterministic.  The "single update epoch on fixed sample lists"
@@ -201,7 +208,8 @@ def apply_sample_lists(M, sources, samples, labels, lr: float, deterministic: bo
     lab = torch.as_tensor(np.asarray(labels, dtype=np.int8)).cuda()
     k = int(smp.shape[1]) if smp.dim() == 2 else 0
     flags = (_lib.GB_TRAIN_EXACT if deterministic else _lib.GB_TRAIN_FAST_SIGMOID) | (
-        _lib.GB_TRAIN_REUSE if reuse_updated_source else 0)
+        _lib.GB_TRAIN_REUSE if reuse_updated_source else 0) | (
+        _lib.GB_TRAIN_ATOMIC if atomic_rows and not deterministic else 0)
     status = _lib.new_status()
     _lib.call("gb_apply_sample_lists", _lib.ptr(dm.dev), dm.dev.shape[1], int(src.numel()),
               _lib.ptr(src), k, _lib.ptr(smp), _lib.ptr(lab), float(lr), flags,

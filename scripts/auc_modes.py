@@ -6,6 +6,7 @@ Modes (MODES env, comma list):
              num_workers=1, i.e. the reference's own AUCROC
   cap<N>     Hogwild with max_inflight=N (cap0 = auto policy)
   tour<R>    finest level by the part-pair tournament over R virtual ranks
+  a suffix "a" (cap0a, tour2a) adds atomic_rows (vector-reduction write-back)
 
     GRAPH=c1|c3 MODES=det,cap0 SEEDS=1 UNIT=vertex-pass EPOCHS=1000 \\
         EVAL_SAMPLE=1000000 python scripts/auc_modes.py
@@ -55,12 +56,15 @@ print(json.dumps({"graph": graph, "vertices": g.num_vertices, "arcs": g.num_edge
                   "eval_train_pairs": 2 * int(pos_train.shape[0]),
                   "eval_test_pairs": 2 * int(pos_test.shape[0]), "unit": unit,
                   "epochs": epochs, "dim": dim}), flush=True)
-for mode in modes:
+for mode_s in modes:
+    atomic = mode_s.endswith("a")
+    mode = mode_s[:-1] if atomic else mode_s
     for seed in seeds:
         cfg = gb.TrainConfig(dim=dim, total_epochs=epochs, smoothing_ratio=0.3,
                              learning_rate=0.035, negative_samples=3, seed=seed,
                              epoch_unit=unit, deterministic=mode == "det",
-                             max_inflight=int(mode[3:]) if mode.startswith("cap") else 0)
+                             max_inflight=int(mode[3:]) if mode.startswith("cap") else 0,
+                             atomic_rows=atomic)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         if mode.startswith("tour"):
@@ -76,7 +80,7 @@ for mode in modes:
         model = gb.train_logreg_device(f_train, gb.LogRegConfig(seed=eval_seed))
         auc = gb.auc_roc_device(gb.predict_scores_device(model, f_test.rows), f_test.labels)
         eval_s = time.perf_counter() - t0
-        print(json.dumps({"mode": mode, "seed": seed, "aucroc": auc, "embed_s": embed_s,
+        print(json.dumps({"mode": mode_s, "seed": seed, "aucroc": auc, "embed_s": embed_s,
                           "eval_s": eval_s}), flush=True)
         del M, f_train, f_test
         torch.cuda.empty_cache()

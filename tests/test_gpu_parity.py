@@ -258,6 +258,36 @@ def test_fixed_sample_lists_parallel_within_tolerance(cuda, orc):
     M2 = M0.copy()
     gb.apply_sample_lists(M2, src, samples, labels, 0.05, deterministic=True)
     assert np.array_equal(M2, ref)
+    M3 = M0.copy()
+    gb.apply_sample_lists(M3, src, samples, labels, 0.05, atomic_rows=True)
+    assert _rel_err(M3, ref) <= REL_TOL
+
+
+def test_atomic_rows_keep_concurrent_updates_of_a_hot_row(cuda, orc):
+    """Every source trains against the same hub row at once: with vector-
+    reduction write-back all increments land (the result matches the
+    sequential order up to second-order staleness); plain stores lose most."""
+    rng = np.random.default_rng(21)
+    V, d, n, hub = 6000, 128, 4096, 5999
+    M0 = orc.init_embedding(V, d, 3) * 40.0
+    src = rng.permutation(V - 1)[:n]
+    samples = np.full((n, 1), hub, dtype=np.int64)
+    labels = np.array([1], dtype=np.int8)
+    lr = 1e-4
+    ref = M0.copy()
+    for i in range(n):
+        orc.update_embedding(ref, int(src[i]), hub, 1, lr)
+    dref = ref[hub].astype(np.float64) - M0[hub]
+    Ma = M0.copy()
+    gb.apply_sample_lists(Ma, src, samples, labels, lr, atomic_rows=True)
+    Ms = M0.copy()
+    gb.apply_sample_lists(Ms, src, samples, labels, lr)
+    err_a = np.abs((Ma[hub] - M0[hub]) - dref).max() / np.abs(dref).max()
+    err_s = np.abs((Ms[hub] - M0[hub]) - dref).max() / np.abs(dref).max()
+    assert err_a < 1e-3, err_a
+    assert err_s > 10 * err_a
+    others = np.setdiff1d(np.arange(V), [hub])
+    assert _rel_err(Ma[others], ref[others]) <= 1e-4
 
 
 def test_hogwild_pass_counts_and_finiteness(cuda, orc):
