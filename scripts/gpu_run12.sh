@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -30 > gpurun_out/pytest_gpu.txt
+timeout 900 python -m pytest tests -q -m gpu 2>&1 | tail -30 > gpurun_out/pytest_gpu.txt
 cat gpurun_out/pytest_gpu.txt
 timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/bench_store.json 2>gpurun_out/bench_store.err; tail -2 gpurun_out/bench_store.err; cat gpurun_out/bench_store.json
 timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --atomic-rows > gpurun_out/bench_atomic.json 2>gpurun_out/bench_atomic.err; tail -2 gpurun_out/bench_atomic.err; cat gpurun_out/bench_atomic.json

@@ -290,6 +290,23 @@ def test_atomic_rows_keep_concurrent_updates_of_a_hot_row(cuda, orc):
     assert _rel_err(Ma[others], ref[others]) <= 1e-4
 
 
+@pytest.mark.parametrize("pipe", ["0", "1"])
+@pytest.mark.parametrize("d", [32, 128])
+def test_single_group_passes_match_sequential(cuda, orc, d, pipe, monkeypatch):
+    """The parallel pass kernels (throughput and latency variants) with one
+    source in flight are the reference's sequential pass up to the tree dot
+    and fp32 sigmoid: within 1e-5 relative after two passes."""
+    monkeypatch.setenv("GB_PIPE", pipe)
+    x, a = orc.rmat_graph(11, 20000, 3, densify_ids=True)
+    g = Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
+    M0 = orc.init_embedding(g.num_vertices, d, 1) * 20.0
+    ref = M0.copy()
+    orc.train_level(x, a, ref, d, 2, 0.035, 3, 1, 0)
+    M = M0.copy()
+    gb.train_level(g, M, gb.TrainConfig(dim=d, max_inflight=1), 2)
+    assert _rel_err(M, ref) <= REL_TOL
+
+
 def test_hogwild_pass_counts_and_finiteness(cuda, orc):
     G = gb.rmat_graph(16, 1 << 20, 2)
     M = torch.from_numpy(orc.init_embedding(G.num_vertices, 128, 1)).cuda()
