@@ -213,7 +213,7 @@ def run_ours(args):
     status = _lib.new_status()
     stream = torch.cuda.current_stream()
     cap = gb.trainer.inflight_cap(gb.TrainConfig(dim=DIM), V)
-    flags = _lib.GB_TRAIN_FAST_SIGMOID | (_lib.GB_TRAIN_ATOMIC if args.atomic_rows else 0)
+    flags = _lib.GB_TRAIN_FAST_SIGMOID | (_lib.GB_TRAIN_ATOMIC if (not args.store_rows) else 0)
 
     def launch(p):
         _lib.call("gb_train_passes", V, _lib.ptr(xadj), _lib.ptr(adj), _lib.ptr(sources),
@@ -260,7 +260,7 @@ def run_ours(args):
     # host memory and back every step.
     M_host = torch.from_numpy(gb.init_embedding(V, DIM, 1)).pin_memory()
     cfg = gb.TrainConfig(dim=DIM, negative_samples=NNEG, seed=1, learning_rate=LR,
-                         epoch_unit="edge-scaled", atomic_rows=args.atomic_rows)
+                         epoch_unit="edge-scaled", atomic_rows=(not args.store_rows))
     e2e_steps = max(2, min(args.steps // 10, 5))
     gb.train_level(G, M_host, cfg, 1)  # warm-up
     torch.cuda.synchronize()
@@ -293,7 +293,7 @@ def run_ours(args):
             "vertices": V, "non_isolated_sources": non_iso, "arcs": G.num_edges,
             "parallelism": "replicas" if world > 1 else "single GPU",
             "inflight_groups_cap": cap, "graph_build_s": round(build_s, 3),
-            "row_writeback": "vector reductions" if args.atomic_rows else "stores"}),
+            "row_writeback": "vector reductions" if (not args.store_rows) else "stores"}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": non_iso * bps,
@@ -328,7 +328,7 @@ def run_tournament(args):
     G = gb.rmat_graph(SCALE, SAMPLES, SEED)
     V = G.num_vertices
     cfg = gb.TrainConfig(dim=DIM, negative_samples=NNEG, seed=1, learning_rate=LR,
-                         atomic_rows=args.atomic_rows)
+                         atomic_rows=(not args.store_rows))
     M = torch.from_numpy(gb.init_embedding(V, DIM, 1)).to(dev)
 
     def step():
@@ -393,8 +393,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", choices=["c2", "tournament"], default="c2")
-    ap.add_argument("--atomic-rows", action="store_true",
-                    help="sample rows written back by vector reductions (GB_TRAIN_ATOMIC)")
+    ap.add_argument("--store-rows", action="store_true",
+                    help="write sample rows back with plain stores instead of the default "
+                         "vector reductions (GB_TRAIN_ATOMIC off)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -705,7 +705,7 @@ __global__ void __launch_bounds__(kBlock, Row::kMinBlocks) train_pool_kernel(Poo
     }
     const uint64_t key = stream_key(a.seed, a.side, 1, (uint64_t)i);
     // positives of pool slots [t_base, t_base + G): lane l holds slot t_base + l
-    int64_t t_base = -1;
+    int64_t t_base = -(int64_t)G;  // empty window: the first slot refills it
     int32_t tgt_lane = -1;
     Row S;
     bool loaded = false;

@@ -61,7 +61,7 @@ class TrainConfig:
     reuse_updated_source: bool = False
     deterministic: bool = False
     max_inflight: int = 0
-    atomic_rows: bool = False
+    atomic_rows: bool = True
 
     def validate(self) -> None:
         if self.dim < 1:
@@ -197,7 +197,7 @@ def update_embedding(M, v: int, s: int, b: int, lr: float,
 
 def apply_sample_lists(M, sources, samples, labels, lr: float, deterministic: bool = False,
                        reuse_updated_source: bool = False, max_inflight: int = 0,
-                       atomic_rows: bool = False) -> None:
+                       atomic_rows: bool = True) -> None:
     """Fixed sample lists: source sources[i] is updated against samples[i, j]
     (j ascending; -1 skips) with label labels[j].  Sources run concurrently
     unless deterministic.  The "single update epoch on fixed sample lists"

@@ -6,7 +6,8 @@ Modes (MODES env, comma list):
              num_workers=1, i.e. the reference's own AUCROC
   cap<N>     Hogwild with max_inflight=N (cap0 = auto policy)
   tour<R>    finest level by the part-pair tournament over R virtual ranks
-  a suffix "a" (cap0a, tour2a) adds atomic_rows (vector-reduction write-back)
+  a suffix "s" (cap0s, tour2s) writes sample rows back with plain stores
+  (atomic_rows=False); the default is vector-reduction write-back
 
     GRAPH=c1|c3 MODES=det,cap0 SEEDS=1 UNIT=vertex-pass EPOCHS=1000 \\
         EVAL_SAMPLE=1000000 python scripts/auc_modes.py
@@ -57,8 +58,8 @@ print(json.dumps({"graph": graph, "vertices": g.num_vertices, "arcs": g.num_edge
                   "eval_test_pairs": 2 * int(pos_test.shape[0]), "unit": unit,
                   "epochs": epochs, "dim": dim}), flush=True)
 for mode_s in modes:
-    atomic = mode_s.endswith("a")
-    mode = mode_s[:-1] if atomic else mode_s
+    atomic = not mode_s.endswith("s")
+    mode = mode_s if atomic else mode_s[:-1]
     for seed in seeds:
         cfg = gb.TrainConfig(dim=dim, total_epochs=epochs, smoothing_ratio=0.3,
                              learning_rate=0.035, negative_samples=3, seed=seed,
