@@ -648,38 +648,8 @@ __device__ __forceinline__ int64_t lower_bound_adj(const int32_t *__restrict__ a
   return lo;
 }
 
-// Group-cooperative lower_bound over adj[lo, hi): each round the G lanes
-// probe G evenly spaced positions and the ballot count of probes below x
-// narrows the range (G+1)-fold, so a row of degree D takes ~log_{G+1} D
-// dependent loads instead of log_2 D.  Every lane returns the same index.
-template <int G>
-__device__ __forceinline__ int64_t group_lower_bound(const int32_t *__restrict__ adj, int64_t lo,
-                                                     int64_t hi, int64_t x, int gl,
-                                                     unsigned gmask) {
-  const int shift = (threadIdx.x & 31) / G * G;
-  while (hi - lo > G) {
-    const int64_t span = hi - lo;
-    const int64_t pos = lo + (span * (gl + 1)) / (G + 1);
-    const bool below = (int64_t)__ldg(adj + pos) < x;
-    const unsigned m = (__ballot_sync(gmask, below) >> shift) & ((G == 32) ? 0xffffffffu : ((1u << G) - 1u));
-    const int c = __popc(m);  // probes below x form a prefix (rows are sorted)
-    const int64_t new_lo = c == 0 ? lo : lo + (span * c) / (G + 1) + 1;
-    const int64_t new_hi = c == G ? hi : lo + (span * (c + 1)) / (G + 1);
-    lo = new_lo;
-    hi = new_hi;
-  }
-  const int64_t pos = lo + gl;
-  const bool below = pos < hi && (int64_t)__ldg(adj + pos) < x;
-  const unsigned m = (__ballot_sync(gmask, below) >> shift) & ((G == 32) ? 0xffffffffu : ((1u << G) - 1u));
-  return lo + __popc(m);
-}
-
-// Per source: the pool side (two cooperative lower bounds, then the B pool
-// draws fetched G at a time, one per lane, and broadcast by shuffle) and
-// B*(1+n_neg) chained updates in chunks of kChunk.
 template <class Row, bool EXACT>
 __global__ void __launch_bounds__(kBlock, Row::kMinBlocks) train_pool_kernel(PoolArgs a) {
-  constexpr int G = Row::G;
   const GroupCtx g = group_ctx<Row>();
   const Slots<Row> sl(a.max_groups);
   if (sl.warp_idle()) return;
@@ -698,15 +668,12 @@ __global__ void __launch_bounds__(kBlock, Row::kMinBlocks) train_pool_kernel(Poo
     if (a.targets == nullptr) {
       const int64_t v = a.lo_s + i;
       const int64_t e0 = __ldg(a.xadj + v), e1 = __ldg(a.xadj + v + 1);
-      first = group_lower_bound<G>(a.adj, e0, e1, a.lo_t, g.gl, g.gmask);
-      cnt = group_lower_bound<G>(a.adj, first, e1, a.lo_t + a.n_t, g.gl, g.gmask) - first;
+      first = lower_bound_adj(a.adj, e0, e1, a.lo_t);
+      cnt = lower_bound_adj(a.adj, first, e1, a.lo_t + a.n_t) - first;
       if (cnt == 0) continue;  // every slot is -1
       pkey = stream_key(a.seed, a.pool_side, 0, (uint64_t)v);
     }
     const uint64_t key = stream_key(a.seed, a.side, 1, (uint64_t)i);
-    // positives of pool slots [t_base, t_base + G): lane l holds slot t_base + l
-    int64_t t_base = -(int64_t)G;  // empty window: the first slot refills it
-    int32_t tgt_lane = -1;
     Row S;
     bool loaded = false;
     for (int64_t c0 = 0; c0 < total; c0 += kChunk) {
@@ -719,18 +686,11 @@ __global__ void __launch_bounds__(kBlock, Row::kMinBlocks) train_pool_kernel(Poo
         if (idx >= total) continue;
         const int64_t t = idx / per_t;
         const int q = (int)(idx - t * per_t);
-        if (t >= t_base + G) {  // uniform across the group: refill the window
-          t_base = t - t % G;
-          const int64_t tl = t_base + g.gl;
-          tgt_lane = -1;
-          if (tl < a.B) {
-            if (a.targets != nullptr)
-              tgt_lane = __ldg(a.targets + i * a.B + tl);
-            else
-              tgt_lane = __ldg(a.adj + first + draw_below(pkey, (uint64_t)tl, cnt));
-          }
-        }
-        const int32_t tgt = __shfl_sync(g.gmask, tgt_lane, (int)(t - t_base), G);
+        int64_t tgt;
+        if (a.targets != nullptr)
+          tgt = __ldg(a.targets + i * a.B + t);
+        else
+          tgt = __ldg(a.adj + first + draw_below(pkey, (uint64_t)t, cnt));
         if (tgt < 0) continue;  // absent slot: no positive, no negatives
         if (q == 0) {
           ids[j] = (int32_t)(tgt - a.lo_t);
