@@ -187,3 +187,24 @@ def test_device_tournament_hogwild_counts(cuda, orc):
     st = tn.train_tournament(g, M, cfg, 2, num_ranks=4)
     assert st["pos_updates"] > 0 and st["neg_updates"] == 3 * st["pos_updates"]
     assert bool(torch.isfinite(M).all())
+
+
+def test_ragged_parts_and_tiny_levels(orc):
+    """Parts of unequal size (V not a multiple of K) and a level barely
+    larger than K still equal the sequential replay; fewer rows than parts
+    is rejected."""
+    x, a = orc.rmat_graph(5, 120, 9, densify_ids=True)
+    g = Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
+    cfg = gb.TrainConfig(dim=8, negative_samples=2, seed=5, deterministic=True)
+    for G in (5, 7):  # V = 24: parts of 2 and 3 rows (K=10), 1 and 2 rows (K=14)
+        assert g.num_vertices % (2 * G) != 0
+        M0 = orc.init_embedding(g.num_vertices, 8, 4)
+        ref = M0.copy()
+        _sequential_replay(orc, g, x, a, ref, cfg, 7, G)
+        M = torch.from_numpy(M0.copy())
+        tn.train_tournament(g, M, cfg, 7, num_ranks=G, pair_fn=_oracle_pair_fn(orc, x, a, 5, 2))
+        assert np.array_equal(M.numpy(), ref)
+    tiny = Graph(3, 4, xadj=np.array([0, 1, 3, 4]), adj=np.array([1, 0, 2, 1], np.int32))
+    with pytest.raises(gb.ConfigError):
+        tn.train_tournament(tiny, torch.zeros(3, 8), cfg, 1, num_ranks=2,
+                            pair_fn=lambda *args: None)
