@@ -42,8 +42,8 @@ LR_FLOOR = 1e-4
 EPOCH_UNITS = ("vertex-pass", "edge-scaled")
 # auto in-flight policy max(FLOOR, V / DIVISOR); the environment overrides
 # exist for staleness/quality experiments (scripts/auc_modes.py)
-INFLIGHT_FLOOR = int(os.environ.get("GB_INFLIGHT_FLOOR", "64"))
-INFLIGHT_DIVISOR = int(os.environ.get("GB_INFLIGHT_DIV", "64"))
+INFLIGHT_FLOOR = int(os.environ.get("GB_INFLIGHT_FLOOR", "256"))
+INFLIGHT_DIVISOR = int(os.environ.get("GB_INFLIGHT_DIV", "16"))
 
 
 @dataclass
@@ -96,7 +96,7 @@ class TrainStats(NamedTuple):
 
 def inflight_cap(cfg: TrainConfig, num_vertices: int) -> int:
     """Sources in flight for a level: 1 when deterministic, the explicit cap
-    when set, else max(64, V/64) -- the staleness bound from SURVEY.md
+    when set, else max(256, V/16) -- the staleness bound from SURVEY.md
     finding 11 (a no-op on large levels, where the GPU holds fewer groups)."""
     if cfg.deterministic:
         return 1
