@@ -121,14 +121,21 @@ struct ScalarRow {
   }
   __device__ __forceinline__ static double serial_dot(const ScalarRow &a, const ScalarRow &b,
                                                       unsigned gmask, int gl, int dim) {
+    // The add chain is inherently serial; the shuffles feeding it are not,
+    // so they are issued in batches of 8 ahead of the adds that consume
+    // them (a shuffle per add on the critical path costs ~4x).
     double acc = 0.0;
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
-      double p = __dmul_rn((double)a.x[k], (double)b.x[k]);
-#pragma unroll 1
-      for (int src = 0; src < 32; ++src) {
-        double q = __shfl_sync(gmask, p, src, 32);
-        if (k * 32 + src < dim) acc = __dadd_rn(acc, q);
+      const double p = __dmul_rn((double)a.x[k], (double)b.x[k]);
+#pragma unroll
+      for (int s0 = 0; s0 < 32; s0 += 8) {
+        double q[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) q[j] = __shfl_sync(gmask, p, s0 + j, 32);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (k * 32 + s0 + j < dim) acc = __dadd_rn(acc, q[j]);
       }
     }
     return acc;
@@ -531,7 +538,7 @@ __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &
 // BATCH = true (latency variant, capped launches): batched-dot chunks and one
 // block per SM worth of registers.
 template <class Row, bool EXACT, bool BATCH>
-__global__ void __launch_bounds__(kBlock, BATCH ? 1 : Row::kMinBlocks)
+__global__ void __launch_bounds__(kBlock, (BATCH || EXACT) ? 1 : Row::kMinBlocks)
     train_passes_kernel(PassArgs a) {
   constexpr int G = Row::G;
   const GroupCtx g = group_ctx<Row>();
@@ -649,7 +656,7 @@ __device__ __forceinline__ int64_t lower_bound_adj(const int32_t *__restrict__ a
 }
 
 template <class Row, bool EXACT>
-__global__ void __launch_bounds__(kBlock, Row::kMinBlocks) train_pool_kernel(PoolArgs a) {
+__global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_pool_kernel(PoolArgs a) {
   const GroupCtx g = group_ctx<Row>();
   const Slots<Row> sl(a.max_groups);
   if (sl.warp_idle()) return;
@@ -741,7 +748,7 @@ struct ListArgs {
 };
 
 template <class Row, bool EXACT>
-__global__ void __launch_bounds__(kBlock, Row::kMinBlocks) apply_lists_kernel(ListArgs a) {
+__global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) apply_lists_kernel(ListArgs a) {
   const GroupCtx g = group_ctx<Row>();
   const Slots<Row> sl(a.max_groups);
   if (sl.warp_idle()) return;
