@@ -132,7 +132,13 @@ def ptr(t: torch.Tensor | None) -> int | None:
 def workspace(query: str, *args) -> tuple[torch.Tensor, int]:
     n = C.c_size_t(0)
     call(query, *args, C.byref(n))
-    ws = torch.empty(max(int(n.value), 1), dtype=torch.uint8, device="cuda")
+    try:
+        ws = torch.empty(max(int(n.value), 1), dtype=torch.uint8, device="cuda")
+    except torch.OutOfMemoryError:
+        # big-graph workspaces (tens of GiB) can fail on cached-but-fragmented
+        # blocks; hand them back to the driver and retry once
+        torch.cuda.empty_cache()
+        ws = torch.empty(max(int(n.value), 1), dtype=torch.uint8, device="cuda")
     return ws, int(n.value)
 
 
