@@ -208,3 +208,44 @@ def test_ragged_parts_and_tiny_levels(orc):
     with pytest.raises(gb.ConfigError):
         tn.train_tournament(tiny, torch.zeros(3, 8), cfg, 1, num_ranks=2,
                             pair_fn=lambda *args: None)
+
+
+def _nccl_worker(rank, world, port, out_path):
+    import torch.distributed as dist
+    from oracle import oracle as orc
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        g, x, a = _graph(orc, scale=10, samples=6000)
+        cfg = gb.TrainConfig(dim=32, total_epochs=30, negative_samples=3, seed=4,
+                             deterministic=True)
+        M, stats = gb.train_multilevel_sharded(g, cfg)
+        np.save(f"{out_path}.{rank}.npy", M)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_process_group_path_equals_virtual_ranks(cuda, orc):
+    """The torch.distributed (NCCL) code path of the sharded multilevel
+    driver -- broadcast, tournament, all_reduce, all_gather -- on the GPUs
+    this box has equals the in-process virtual-rank run bit for bit."""
+    import socket
+
+    import torch.multiprocessing as mp
+    world = torch.cuda.device_count()
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "m")
+        mp.spawn(_nccl_worker, args=(world, port, out), nprocs=world, join=True)
+        g, x, a = _graph(orc, scale=10, samples=6000)
+        cfg = gb.TrainConfig(dim=32, total_epochs=30, negative_samples=3, seed=4,
+                             deterministic=True)
+        ref, _ = gb.train_multilevel_sharded(g, cfg, num_ranks=world)
+        for r in range(world):
+            assert np.array_equal(np.load(f"{out}.{r}.npy"), ref)
