@@ -683,28 +683,37 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
     const uint64_t key = stream_key(a.seed, a.side, 1, (uint64_t)i);
     Row S;
     bool loaded = false;
+    // (slot t, sample q) of flat index c0 + j, advanced incrementally (no
+    // 64-bit division per sample)
+    int64_t t_cur = 0;
+    int q_cur = 0;
     for (int64_t c0 = 0; c0 < total; c0 += kChunk) {
       int32_t ids[kChunk];
       unsigned pos_mask = 0;
 #pragma unroll
       for (int j = 0; j < kChunk; ++j) {
-        const int64_t idx = c0 + j;
-        ids[j] = -1;
-        if (idx >= total) continue;
-        const int64_t t = idx / per_t;
-        const int q = (int)(idx - t * per_t);
-        int64_t tgt;
-        if (a.targets != nullptr)
-          tgt = __ldg(a.targets + i * a.B + t);
-        else
-          tgt = __ldg(a.adj + first + draw_below(pkey, (uint64_t)t, cnt));
-        if (tgt < 0) continue;  // absent slot: no positive, no negatives
-        if (q == 0) {
-          ids[j] = (int32_t)(tgt - a.lo_t);
-          pos_mask |= 1u << j;
-        } else {
-          ids[j] = (int32_t)draw_below(key, (uint64_t)(t * a.n_neg + (q - 1)), a.n_t);
+        const int64_t t = t_cur;
+        const int q = q_cur;
+        if (++q_cur == per_t) {
+          q_cur = 0;
+          ++t_cur;
         }
+        ids[j] = -1;
+        if (c0 + j >= total) continue;
+        if (a.targets != nullptr) {
+          const int64_t tgt = __ldg(a.targets + i * a.B + t);
+          if (tgt < 0) continue;  // absent slot: no positive, no negatives
+          if (q == 0) {
+            ids[j] = (int32_t)(tgt - a.lo_t);
+            pos_mask |= 1u << j;
+            continue;
+          }
+        } else if (q == 0) {  // fused pool: cnt > 0, so no slot is absent
+          ids[j] = (int32_t)(__ldg(a.adj + first + draw_below(pkey, (uint64_t)t, cnt)) - a.lo_t);
+          pos_mask |= 1u << j;
+          continue;
+        }
+        ids[j] = (int32_t)draw_below(key, (uint64_t)(t * a.n_neg + (q - 1)), a.n_t);
       }
       if (!(ids[0] >= 0 || ids[1] >= 0 || ids[2] >= 0 || ids[3] >= 0)) continue;
       if (!loaded) {

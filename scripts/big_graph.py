@@ -15,6 +15,12 @@ import os
 import sys
 import time
 
+# Transient workspaces here are tens of GiB; with torch's default caching
+# allocator a long-lived tensor placed inside a freed workspace segment pins
+# it (112 GiB reserved-but-unusable at scale 27).  The driver's stream-ordered
+# pool has no such fragmentation and allocates as fast.
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "backend:cudaMallocAsync")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
