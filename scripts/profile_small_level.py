@@ -32,7 +32,8 @@ for cap in caps:
     def run(n):
         _lib.call("gb_train_passes", V, _lib.ptr(xadj), _lib.ptr(adj), _lib.ptr(srcs), n_src,
                   _lib.ptr(M), dim, 3, 1, 0, 0, n, 1 << 40, _lib.ptr(lrs),
-                  _lib.GB_TRAIN_FAST_SIGMOID, cap, _lib.ptr(st), _lib.stream())
+                  _lib.GB_TRAIN_FAST_SIGMOID | _lib.GB_TRAIN_ATOMIC, cap, _lib.ptr(st),
+                  _lib.stream())
     if os.environ.get("NCU"):
         run(20)
         run(20)
