@@ -280,30 +280,21 @@ __device__ __forceinline__ GroupCtx group_ctx() {
   return c;
 }
 
-// Gathers the sample rows of a chunk (a sample equal to the source is not
-// loaded when self_possible: the register copy of the source is used).
-template <class Row>
-__device__ __forceinline__ void load_chunk_rows(Row (&R)[kChunk], int64_t src_row,
-                                                const int32_t (&ids)[kChunk],
-                                                const float *__restrict__ Mtgt, int dim,
-                                                bool self_possible, int gl) {
+// Runs one chunk of up to kChunk samples against the register-resident
+// source S.  ids[j] < 0 marks an unused slot; bit j of pos_mask marks a
+// positive (b = 1).  Sample rows are gathered first, then updated in order
+// with forwarding of repeated ids, and stored right after their update.
+template <class Row, bool EXACT>
+__device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t (&ids)[kChunk],
+                                          unsigned pos_mask, float *__restrict__ Mtgt, int dim,
+                                          double lr, bool reuse, bool self_possible,
+                                          bool load_once, const GroupCtx &g, bool &bad,
+                                          bool fast = false, bool atomic = false) {
+  Row R[kChunk];
 #pragma unroll
   for (int j = 0; j < kChunk; ++j)
     if (ids[j] >= 0 && !(self_possible && ids[j] == src_row))
-      R[j].load(Mtgt + (int64_t)ids[j] * dim, gl, dim);
-}
-
-// Sequential updates of a chunk whose rows are already in R: the
-// reference's order, forwarding of repeated ids, aliasing rule for s == v,
-// each sample row written back right after its update.
-template <class Row, bool EXACT>
-__device__ __forceinline__ void run_chunk_loaded(Row &S, int64_t src_row,
-                                                 const int32_t (&ids)[kChunk], unsigned pos_mask,
-                                                 Row (&R)[kChunk], float *__restrict__ Mtgt,
-                                                 int dim, double lr, bool reuse,
-                                                 bool self_possible, bool load_once,
-                                                 const GroupCtx &g, bool &bad, bool fast,
-                                                 bool atomic) {
+      R[j].load(Mtgt + (int64_t)ids[j] * dim, g.gl, dim);
 #pragma unroll
   for (int j = 0; j < kChunk; ++j) {
     const int32_t s = ids[j];
@@ -325,25 +316,23 @@ __device__ __forceinline__ void run_chunk_loaded(Row &S, int64_t src_row,
   }
 }
 
-// Runs one chunk of up to kChunk samples against the register-resident
-// source S.  ids[j] < 0 marks an unused slot; bit j of pos_mask marks a
-// positive (b = 1).  Sample rows are gathered first, then updated in order
-// with forwarding of repeated ids, and stored right after their update.
-template <class Row, bool EXACT>
-__device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t (&ids)[kChunk],
-                                          unsigned pos_mask, float *__restrict__ Mtgt, int dim,
-                                          double lr, bool reuse, bool self_possible,
-                                          bool load_once, const GroupCtx &g, bool &bad,
-                                          bool fast = false, bool atomic = false) {
-  Row R[kChunk];
-  load_chunk_rows(R, src_row, ids, Mtgt, dim, self_possible, g.gl);
-  run_chunk_loaded<Row, EXACT>(S, src_row, ids, pos_mask, R, Mtgt, dim, lr, reuse,
-                               self_possible, load_once, g, bad, fast, atomic);
-}
-
-// True when the chunk's sample ids are pairwise distinct and all differ
-// from the source: the precondition of the batched (Gram) update.
-__device__ __forceinline__ bool chunk_is_simple(int64_t src_row, const int32_t (&ids)[kChunk]) {
+// Batched-dot chunk (non-exact, latency variant).  With distinct sample ids
+// that all differ from the source, S before update k is
+// S + sum_{j<k} sc_j R_j, so the k-th dot is
+//   d_k = S.R_k + sum_{j<k} sc_j (R_j.R_k)
+// -- all 4 + 6 fp64 dot products are independent and reduce together (one
+// butterfly, full ILP); only a short scalar chain of sigmoids remains.  The
+// row updates are then applied element by element in the reference's order
+// (identical fp32 operations).  d_k differs from the dot of the fp32-rounded
+// updated row by rounding only (~1e-7 relative), within the 1e-5 bar.
+// Returns false (nothing done) when ids repeat or hit the source; the caller
+// then takes the sequential path.
+template <class Row>
+__device__ __forceinline__ bool batched_chunk(Row &S, int64_t src_row, const int32_t (&ids)[kChunk],
+                                              unsigned pos_mask, float *__restrict__ Mtgt,
+                                              int dim, double lr, bool reuse, const GroupCtx &g,
+                                              bool &bad, bool fast, bool atomic = false) {
+  static_assert(kChunk == 4, "batched_chunk assumes 4 samples");
   bool simple = true;
 #pragma unroll
   for (int j = 0; j < kChunk; ++j) {
@@ -352,16 +341,11 @@ __device__ __forceinline__ bool chunk_is_simple(int64_t src_row, const int32_t (
     for (int k = j + 1; k < kChunk; ++k)
       if (ids[j] >= 0 && ids[j] == ids[k]) simple = false;
   }
-  return simple;
-}
-
-template <class Row>
-__device__ __forceinline__ void batched_chunk_loaded(Row &S, const int32_t (&ids)[kChunk],
-                                                     unsigned pos_mask, Row (&R)[kChunk],
-                                                     float *__restrict__ Mtgt, int dim,
-                                                     double lr, bool reuse, const GroupCtx &g,
-                                                     bool &bad, bool fast, bool atomic) {
-  static_assert(kChunk == 4, "batched_chunk assumes 4 samples");
+  if (!simple) return false;
+  Row R[kChunk];
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j)
+    if (ids[j] >= 0) R[j].load(Mtgt + (int64_t)ids[j] * dim, g.gl, dim);
   // 10 partial dots: q[j] = S.R_j, q[4 + pair(j,k)] = R_j.R_k (j < k)
   double q[10];
 #pragma unroll
@@ -406,28 +390,6 @@ __device__ __forceinline__ void batched_chunk_loaded(Row &S, const int32_t (&ids
     update_pair_writeback(S, R[j], sc[j], reuse, atomic, Mtgt + (int64_t)ids[j] * dim, g.gl,
                           dim);
   }
-}
-
-// Batched-dot chunk (non-exact, latency variant).  With distinct sample ids
-// that all differ from the source, S before update k is
-// S + sum_{j<k} sc_j R_j, so the k-th dot is
-//   d_k = S.R_k + sum_{j<k} sc_j (R_j.R_k)
-// -- all 4 + 6 fp64 dot products are independent and reduce together (one
-// butterfly, full ILP); only a short scalar chain of sigmoids remains.  The
-// row updates are then applied element by element in the reference's order
-// (identical fp32 operations).  d_k differs from the dot of the fp32-rounded
-// updated row by rounding only (~1e-7 relative), within the 1e-5 bar.
-// Returns false (nothing done) when ids repeat or hit the source; the caller
-// then takes the sequential path.
-template <class Row>
-__device__ __forceinline__ bool batched_chunk(Row &S, int64_t src_row, const int32_t (&ids)[kChunk],
-                                              unsigned pos_mask, float *__restrict__ Mtgt,
-                                              int dim, double lr, bool reuse, const GroupCtx &g,
-                                              bool &bad, bool fast, bool atomic = false) {
-  if (!chunk_is_simple(src_row, ids)) return false;
-  Row R[kChunk];
-  load_chunk_rows(R, src_row, ids, Mtgt, dim, false, g.gl);
-  batched_chunk_loaded(S, ids, pos_mask, R, Mtgt, dim, lr, reuse, g, bad, fast, atomic);
   return true;
 }
 
@@ -566,74 +528,6 @@ __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &
   }
 }
 
-// Replace a prefetched row of the next source by the value the current
-// source just wrote, if it is one of its rows (the source row, or the last
-// copy of a sample row -- repeated ids were forwarded in order).
-template <class Row>
-__device__ __forceinline__ void forward_written(int32_t id, Row &dst, const SourceIdx &d,
-                                                const Row &S, const Row (&R)[kChunk]) {
-  if (id == d.v) dst = S;
-#pragma unroll
-  for (int j = 0; j < kChunk; ++j)
-    if (d.ids[j] >= 0 && d.ids[j] != d.v && d.ids[j] == id) dst = R[j];
-}
-
-// The G sources of an index batch (one chunk each), software-pipelined: the
-// rows of source k+1 are gathered while source k computes, then patched
-// with whatever source k wrote to the same rows, so every source still sees
-// its predecessors' updates exactly as in the one-at-a-time loop (other
-// groups' updates are Hogwild, as always).  Latency variant only: small
-// levels are bound by the per-source load -> dot -> write chain.
-template <class Row>
-__device__ __forceinline__ void train_sources_pipelined(const PassArgs &a, const GroupCtx &g,
-                                                        const SourceIdx &mine, int kmax,
-                                                        bool &bad, int &first_bad) {
-  constexpr int G = Row::G;
-  SourceIdx d = shfl_source(mine, 0, g.gmask, G);
-  Row S, R[kChunk];
-  if (d.active) {
-    S.load(a.M + (int64_t)d.v * a.dim, g.gl, a.dim);
-    load_chunk_rows(R, d.v, d.ids, a.M, a.dim, true, g.gl);
-  }
-  for (int k = 0; k < kmax; ++k) {
-    SourceIdx dn;
-    dn.active = false;
-    Row Sn, Rn[kChunk];
-    if (k + 1 < kmax) {
-      dn = shfl_source(mine, k + 1, g.gmask, G);
-      if (dn.active) {
-        Sn.load(a.M + (int64_t)dn.v * a.dim, g.gl, a.dim);
-        load_chunk_rows(Rn, dn.v, dn.ids, a.M, a.dim, true, g.gl);
-      }
-    }
-    if (d.active) {
-      const double lr = (double)d.lr;
-      bool bad_src = false;
-      if (chunk_is_simple(d.v, d.ids))
-        batched_chunk_loaded(S, d.ids, 1u, R, a.M, a.dim, lr, a.reuse, g, bad_src, a.fast,
-                             a.atomic);
-      else
-        run_chunk_loaded<Row, false>(S, d.v, d.ids, 1u, R, a.M, a.dim, lr, a.reuse, true,
-                                     false, g, bad_src, a.fast, a.atomic);
-      S.store(a.M + (int64_t)d.v * a.dim, g.gl, a.dim);
-      if (bad_src) {
-        bad = true;
-        first_bad = min(first_bad, d.epoch);
-      }
-      if (dn.active) {
-        forward_written(dn.v, Sn, d, S, R);
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j)
-          if (dn.ids[j] >= 0 && dn.ids[j] != dn.v) forward_written(dn.ids[j], Rn[j], d, S, R);
-      }
-    }
-    d = dn;
-    S = Sn;
-#pragma unroll
-    for (int j = 0; j < kChunk; ++j) R[j] = Rn[j];
-  }
-}
-
 // Each group walks a sequence of steps s = 0, 1, ...: step s is pass
 // pass_begin + s / spp, item warp_base + (s % spp)*eff + (its slot), with spp
 // (steps per pass) uniform across the warp so its groups stay in lockstep.
@@ -708,12 +602,6 @@ __global__ void __launch_bounds__(kBlock, (BATCH || EXACT) ? 1 : Row::kMinBlocks
         fetch_source(a, a.pass_begin + q, i, s < total && sl.enabled && i < n, mine);
       }
       const int kmax = (int)(total - s0 < G ? total - s0 : G);
-      if constexpr (!EXACT && Row::E <= 4) {  // two row sets in registers
-        if (a.n_neg + 1 <= kChunk) {
-          train_sources_pipelined<Row>(a, g, mine, kmax, bad, first_bad);
-          continue;
-        }
-      }
       for (int k = 0; k < kmax; ++k) {
         const SourceIdx d = shfl_source(mine, k, g.gmask, G);
         if (d.active) train_source<Row, EXACT, BATCH>(a, g, d, bad, first_bad);
