@@ -198,6 +198,12 @@ int gb_train_pool_side(float *Msrc, float *Mtgt, int dim,
                        unsigned flags, int64_t max_groups, int64_t *status,
                        void *stream_handle);
 
+/* Page-lock a caller host buffer in place (cudaHostRegister) so part
+ * switches of the partitioned trainer DMA straight from / into the caller's
+ * embedding matrix (bigtrain.py:275-299 host staging) without a pinned copy. */
+int gb_host_register(void *ptr, size_t bytes);
+int gb_host_unregister(void *ptr);
+
 /* ---- L4: link-prediction evaluator (evaluate.py), SURVEY.md 8(f) rank 1 ----
  * hadamard_features (evaluate.py:69-78): X[i*dim+t] = fl32(M[u_i,t]*M[v_i,t])
  * for pairs[2i]=u_i, pairs[2i+1]=v_i. */

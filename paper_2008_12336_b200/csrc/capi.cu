@@ -46,3 +46,16 @@ GB_API int gb_device_info(int device, int *num_sms, int *max_warps_per_sm) {
   *max_warps_per_sm = thr / 32;
   return GB_OK;
 }
+
+GB_API int gb_host_register(void *ptr, size_t bytes) {
+  GB_REQUIRE(ptr && bytes > 0, "gb_host_register: bad args");
+  GB_CUDA_TRY(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+  return GB_OK;
+}
+
+GB_API int gb_host_unregister(void *ptr) {
+  GB_REQUIRE(ptr, "gb_host_unregister: null pointer");
+  GB_CUDA_TRY(cudaHostUnregister(ptr));
+  return GB_OK;
+}
+
