@@ -415,3 +415,42 @@ def test_train_large_device_matrix_hogwild(cuda, orc):
     budget = gb.MemoryBudget(3 * 32 * 4 * (G.num_vertices // 4 + 1) + 4 * 2 * 5 * 4 * G.num_vertices)
     st = gb.train_large(G, M, cfg, 10, budget)
     assert st["K"] >= 3 and st["pos_updates"] > 0 and torch.isfinite(M).all()
+
+
+def test_train_large_async_staging_equals_pair_replay(cuda, orc):
+    """train_large with many switches through the side-stream stager (2 slots,
+    K >= 6, 3 rotations, host matrix page-locked in place) equals the
+    sequential replay of its pair schedule by the oracle's pool/pair kernels:
+    staging order and slot reuse cannot change the result."""
+    x, a = orc.rmat_graph(13, 60000, 11, densify_ids=True)
+    G = Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
+    d, B, n_s = 32, 3, 2
+    V = G.num_vertices
+    per_row = 2 * d * 4 + 4 * 2 * B * 4
+    budget = gb.MemoryBudget(per_row * (-(-V // 7)) + 64, parts_resident=2, batch_size=B)
+    cfg = gb.TrainConfig(dim=d, negative_samples=n_s, seed=9, deterministic=True)
+    plan = gb.plan_partitions(V, d, budget)
+    e_i = 3 * B * plan.K
+    M0 = orc.init_embedding(V, d, 2)
+    M = M0.copy()
+    st = gb.train_large(G, M, cfg, e_i, budget)
+    assert st["K"] == plan.K >= 6 and st["rotations"] == 3 and st["switches"] > 3 * plan.K
+    ref = M0.copy()
+    pairs = gb.rotation_pairs(plan.K)
+    for r in range(3):
+        lr = gb.lr_at(cfg.learning_rate, r, 3)
+        for i, (pa, pb) in enumerate(pairs):
+            seed = gb.bigtrain._derived_seed(cfg.seed, 0, r * len(pairs) + i)
+            la, ha = plan.part_range(pa)
+            lb, hb = plan.part_range(pb)
+            A = np.ascontiguousarray(ref[la:ha])
+            Bm = A if pa == pb else np.ascontiguousarray(ref[lb:hb])
+            tj = orc.fill_pool_side(x, a, la, ha, lb, hb, B, seed, 0)
+            orc.train_pool_side(A, Bm, tj, lb, hb - lb, n_s, lr, seed, 2)
+            if pa != pb:
+                tk = orc.fill_pool_side(x, a, lb, hb, la, ha, B, seed, 1)
+                orc.train_pool_side(Bm, A, tk, la, ha - la, n_s, lr, seed, 3)
+            ref[la:ha] = A
+            if pa != pb:
+                ref[lb:hb] = Bm
+    assert np.array_equal(M, ref)
