@@ -454,3 +454,60 @@ def test_train_large_async_staging_equals_pair_replay(cuda, orc):
             if pa != pb:
                 ref[lb:hb] = Bm
     assert np.array_equal(M, ref)
+
+
+# -- reference behaviours at the API edges (test_trainer.py:194-211,
+# test_acceptance.py:203-240, test_bigtrain.py) ------------------------------------
+def _planted(blocks, size, p_in, p_out, seed):
+    rng = np.random.default_rng(seed)
+    n = blocks * size
+    iu, ju = np.triu_indices(n, 1)
+    same = (iu // size) == (ju // size)
+    keep = rng.random(iu.shape[0]) < np.where(same, p_in, p_out)
+    return gb.from_edges(np.column_stack([iu[keep], ju[keep]]), num_vertices=n)
+
+
+def test_train_multilevel_zero_epochs(cuda):
+    g = _planted(6, 12, 0.5, 0.02, 9)
+    cfg = gb.TrainConfig(dim=8, total_epochs=0, seed=3)
+    M = gb.train_multilevel(g, cfg, no_coarsen=True)
+    assert np.array_equal(M, gb.init_embedding(g.num_vertices, 8, 3))
+    h = gb.coarsen_all(g, threshold=4)
+    M = gb.train_multilevel(g, cfg, hierarchy=h)
+    lab = h.mappings[0].map
+    for c in range(h.mappings[0].num_clusters):  # expansion ties cluster rows
+        rows = M[lab == c]
+        assert np.array_equal(rows, np.repeat(rows[:1], rows.shape[0], 0))
+
+
+def test_shape_mismatches_are_rejected(cuda):
+    g = _planted(4, 10, 0.5, 0.05, 2)
+    h = gb.coarsen_all(g, threshold=4)
+    with pytest.raises(ValueError):
+        gb.expand_embedding(np.zeros((h.mappings[0].num_clusters + 1, 8), np.float32),
+                            h.mappings[0])
+    with pytest.raises(ValueError):
+        gb.train_large(g, np.zeros((g.num_vertices + 1, 8), np.float32), gb.TrainConfig(dim=8),
+                       1, gb.MemoryBudget(10**6))
+    with pytest.raises(ValueError):
+        gb.train_level(g, np.zeros((g.num_vertices - 1, 8), np.float32), gb.TrainConfig(dim=8),
+                       1)
+
+
+def test_out_of_core_fidelity(cuda):
+    """Criterion 06 (test_acceptance.py:203-225): link-prediction AUCROC with
+    the level forced out of core (K=3 and K=5 parts) stays within 2 points
+    of the in-memory run."""
+    g = _planted(60, 32, 0.25, 0.01, 7)
+    cfg = gb.TrainConfig(dim=32, total_epochs=200, smoothing_ratio=0.5, learning_rate=0.025,
+                         seed=1, epoch_unit="edge-scaled")
+    base = gb.run_link_prediction(g, cfg, eval_seed=11, evaluator="device").aucroc
+    assert base > 0.8
+    n_train = gb.split_train_test(g, 0.2, 11).train_graph.num_vertices
+    for K in (3, 5):
+        per_row = 3 * 32 * 4 + 4 * 2 * 5 * 4
+        budget = gb.MemoryBudget(per_row * (-(-n_train // K)) + 4096)
+        assert gb.plan_partitions(n_train, 32, budget).K == K
+        auc = gb.run_link_prediction(g, cfg, eval_seed=11, budget=budget,
+                                     evaluator="device").aucroc
+        assert abs(auc - base) <= 0.02, (K, auc, base)
