@@ -498,7 +498,7 @@ def test_out_of_core_fidelity(cuda):
     """Criterion 06 (test_acceptance.py:203-225): link-prediction AUCROC with
     the level forced out of core (K=3 and K=5 parts) stays within 2 points
     of the in-memory run."""
-    g = _planted(60, 32, 0.25, 0.01, 7)
+    g = _planted(60, 32, 0.3, 0.001, 7)
     cfg = gb.TrainConfig(dim=32, total_epochs=200, smoothing_ratio=0.5, learning_rate=0.025,
                          seed=1, epoch_unit="edge-scaled")
     base = gb.run_link_prediction(g, cfg, eval_seed=11, evaluator="device").aucroc
