@@ -204,6 +204,41 @@ int gb_train_pool_side(float *Msrc, float *Mtgt, int dim,
 int gb_host_register(void *ptr, size_t bytes);
 int gb_host_unregister(void *ptr);
 
+/* ---- L5: split and negative pairs (graph.py:46-59, 222-265;
+ * evaluate.py:80-125), SURVEY.md 8(f) rank 3.  The random choices stay
+ * numpy's (host); these do the O(|E|) work around them.
+ * undirected_pairs: arcs (u, v) with u < v in CSR order into pu/pv
+ * (capacity entries); *num_pairs set (synchronizes the stream). */
+int gb_undirected_pairs_workspace(int64_t num_vertices, size_t *bytes);
+int gb_undirected_pairs(const int64_t *xadj, const int32_t *adj,
+                        int64_t num_vertices, int64_t *pu, int64_t *pv,
+                        int64_t capacity, int64_t *num_pairs, void *workspace,
+                        size_t workspace_bytes, void *stream_handle);
+
+/* split_train_test's partition: pairs chosen[k] (indices into pu/pv) are
+ * withheld; vertices touched by the remaining pairs are kept and relabelled
+ * densely in ascending order (relabel[V]: new id or -1; kept[]: old ids);
+ * train pairs (relabelled) and the test pairs whose endpoints both survive
+ * (relabelled) are compacted in pair order.  counts (host) = {train pairs,
+ * test pairs, kept vertices}; synchronizes the stream. */
+int gb_split_partition_workspace(int64_t num_pairs, int64_t num_vertices,
+                                 size_t *bytes);
+int gb_split_partition(const int64_t *pu, const int64_t *pv, int64_t num_pairs,
+                       const int64_t *chosen, int64_t k, int64_t num_vertices,
+                       int64_t *train_u, int64_t *train_v, int64_t *test_u,
+                       int64_t *test_v, int64_t *relabel, int64_t *kept,
+                       int64_t *counts, void *workspace, size_t workspace_bytes,
+                       void *stream_handle);
+
+/* out[i] = 1 iff (u[i], v[i]) is an arc or (u, v) / (v, u) is one of the
+ * excluded pairs -- sample_negative_edges' rejection test. */
+int gb_pairs_member_workspace(int64_t num_excluded, size_t *bytes);
+int gb_pairs_member(const int64_t *xadj, const int32_t *adj, int64_t num_vertices,
+                    const int64_t *u, const int64_t *v, int64_t n,
+                    const int64_t *excl_u, const int64_t *excl_v,
+                    int64_t num_excluded, uint8_t *out, void *workspace,
+                    size_t workspace_bytes, void *stream_handle);
+
 /* ---- L4: link-prediction evaluator (evaluate.py), SURVEY.md 8(f) rank 1 ----
  * hadamard_features (evaluate.py:69-78): X[i*dim+t] = fl32(M[u_i,t]*M[v_i,t])
  * for pairs[2i]=u_i, pairs[2i+1]=v_i. */

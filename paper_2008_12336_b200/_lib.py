@@ -64,6 +64,13 @@ SIGNATURES = {
                                   _u64, _p, _p, _i64, _u64, C.c_uint, _i64, _p, _p]),
     "gb_host_register": (_int, [_p, _sz]),
     "gb_host_unregister": (_int, [_p]),
+    "gb_undirected_pairs_workspace": (_int, [_i64, _psz]),
+    "gb_undirected_pairs": (_int, [_p, _p, _i64, _p, _p, _i64, _pi64, _p, _sz, _p]),
+    "gb_split_partition_workspace": (_int, [_i64, _i64, _psz]),
+    "gb_split_partition": (_int, [_p, _p, _i64, _p, _i64, _i64, _p, _p, _p, _p, _p, _p, _pi64,
+                                  _p, _sz, _p]),
+    "gb_pairs_member_workspace": (_int, [_i64, _psz]),
+    "gb_pairs_member": (_int, [_p, _p, _i64, _p, _p, _i64, _p, _p, _i64, _p, _p, _sz, _p]),
     "gb_hadamard_features": (_int, [_p, _i64, _int, _p, _i64, _p, _p]),
     "gb_logreg_epoch": (_int, [_p, _int, _p, _p, _i64, _int, _dbl, _p, _p, _p]),
     "gb_predict_scores": (_int, [_p, _int, _i64, _p, _dbl, _p, _p]),

@@ -130,7 +130,12 @@ class Graph:
         return np.diff(self.xadj).astype(np.int64)
 
     def undirected_pairs(self) -> np.ndarray:
-        """Arcs (u, v) with u < v as an (m, 2) array; each undirected edge once."""
+        """Arcs (u, v) with u < v as an (m, 2) array in CSR order; each
+        undirected edge once (graph.py:52-59).  Enumerated on the GPU
+        (gb_undirected_pairs) when the CSR lives there."""
+        if self.on_device and self.num_edges > 0:
+            pu, pv, m = _undirected_pairs_device(self)
+            return np.stack([pu[:m].cpu().numpy(), pv[:m].cpu().numpy()], axis=1)
         src = np.repeat(np.arange(self.num_vertices, dtype=np.int64), np.diff(self.xadj))
         dst = self.adj.astype(np.int64)
         m = src < dst
@@ -303,37 +308,63 @@ def load_graph(path: str, directed: bool = False) -> Graph:
     return g
 
 
+def _undirected_pairs_device(g: Graph) -> tuple[torch.Tensor, torch.Tensor, int]:
+    """(pu, pv, m): the u < v arcs of g's device CSR in CSR order."""
+    xadj, adj = g.device_csr()
+    ws, wsb = _lib.workspace("gb_undirected_pairs_workspace", g.num_vertices)
+    m_c = C.c_int64(0)
+    # a symmetric CSR without self-loops has exactly E/2 such arcs; anything
+    # else is retried at the E upper bound
+    for cap in (g.num_edges // 2 + 1, max(g.num_edges, 1)):
+        pu = torch.empty(cap, dtype=torch.int64, device="cuda")
+        pv = torch.empty(cap, dtype=torch.int64, device="cuda")
+        rc = _lib.load().gb_undirected_pairs(_lib.ptr(xadj), _lib.ptr(adj), g.num_vertices,
+                                             _lib.ptr(pu), _lib.ptr(pv), cap, C.byref(m_c),
+                                             _lib.ptr(ws), wsb, _lib.stream())
+        if rc == _lib.GB_OK:
+            return pu, pv, int(m_c.value)
+        del pu, pv
+    _lib.check(rc, "gb_undirected_pairs")
+
+
 def split_train_test(g: Graph, test_fraction: float, seed: int) -> SplitResult:
     """Withhold round(fraction * m) undirected edges chosen by numpy PCG64
-    (same draw as graph.py:242-244), drop vertices left isolated and
-    re-densify; test edges losing an endpoint are dropped (graph.py:222-265).
-    The train CSR is built on the GPU."""
+    (the same draw as graph.py:242-244, on the host), drop vertices left
+    isolated and re-densify; test edges losing an endpoint are dropped
+    (graph.py:222-265).  The pair enumeration, partition, relabelling and
+    the train CSR run on the GPU (csrc/split.cu, csrc/graph.cu)."""
     if g.directed:
         raise SplitError("split requires an undirected graph")
     if not 0.0 < test_fraction < 1.0:
         raise SplitError(f"test_fraction must be in (0, 1), got {test_fraction}")
-    pairs = g.undirected_pairs()
-    m = pairs.shape[0]
+    _lib.require_cuda()
+    V = g.num_vertices
+    st = _lib.stream()
+    pu, pv, m = _undirected_pairs_device(g)
     k = int(round(test_fraction * m))
     if k < 1:
         raise SplitError(f"graph too small to withhold any edge "
                          f"({m} edges at fraction {test_fraction})")
     if k >= m:
         raise SplitError("withholding would leave no training edges")
-    chosen = np.random.default_rng(seed).choice(m, size=k, replace=False)
-    is_test = np.zeros(m, dtype=bool)
-    is_test[chosen] = True
-    train, test = pairs[~is_test], pairs[is_test]
-    used = np.zeros(g.num_vertices, dtype=bool)
-    used[train.ravel()] = True
-    kept = np.flatnonzero(used)
-    relabel = np.full(g.num_vertices, -1, dtype=np.int64)
-    relabel[kept] = np.arange(kept.shape[0])
-    tr = relabel[train]
-    orig = g.orig_ids[kept] if g.orig_ids is not None else kept.copy()
-    tg = _csr_device(int(kept.shape[0]), torch.from_numpy(np.ascontiguousarray(tr[:, 0])),
-                     torch.from_numpy(np.ascontiguousarray(tr[:, 1])),
+    chosen = torch.from_numpy(np.random.default_rng(seed).choice(m, size=k, replace=False)
+                              .astype(np.int64)).cuda()
+    tu = torch.empty(m, dtype=torch.int64, device="cuda")
+    tv = torch.empty(m, dtype=torch.int64, device="cuda")
+    su = torch.empty(k, dtype=torch.int64, device="cuda")
+    sv = torch.empty(k, dtype=torch.int64, device="cuda")
+    relabel = torch.empty(V, dtype=torch.int64, device="cuda")
+    kept = torch.empty(V, dtype=torch.int64, device="cuda")
+    counts = (C.c_int64 * 3)()
+    ws, wsb = _lib.workspace("gb_split_partition_workspace", m, V)
+    _lib.call("gb_split_partition", _lib.ptr(pu[:m]), _lib.ptr(pv[:m]), m, _lib.ptr(chosen), k,
+              V, _lib.ptr(tu), _lib.ptr(tv), _lib.ptr(su), _lib.ptr(sv), _lib.ptr(relabel),
+              _lib.ptr(kept), counts, _lib.ptr(ws), wsb, st)
+    del ws, pu, pv, chosen, relabel
+    n_train, n_test, n_kept = int(counts[0]), int(counts[1]), int(counts[2])
+    kept_h = kept[:n_kept].cpu().numpy()
+    orig = g.orig_ids[kept_h] if g.orig_ids is not None else kept_h.copy()
+    tg = _csr_device(n_kept, tu[:n_train], tv[:n_train],
                      _lib.GB_CSR_DROP_SELF | _lib.GB_CSR_SYMMETRIZE, False, orig_ids=orig)
-    te = relabel[test]
-    te = te[(te >= 0).all(axis=1)]
-    return SplitResult(train_graph=tg, test_edges=te, kept_vertices=kept)
+    te = np.stack([su[:n_test].cpu().numpy(), sv[:n_test].cpu().numpy()], axis=1)
+    return SplitResult(train_graph=tg, test_edges=te, kept_vertices=kept_h)

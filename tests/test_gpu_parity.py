@@ -511,3 +511,57 @@ def test_out_of_core_fidelity(cuda):
         auc = gb.run_link_prediction(g, cfg, eval_seed=11, budget=budget,
                                      evaluator="device").aucroc
         assert abs(auc - base) <= 0.02, (K, auc, base)
+
+
+# -- split and negative pairs on the device ----------------
+def _host_split(g, frac, seed):
+    """graph.py:222-265 restated in numpy (the reference's algorithm)."""
+    x, a = g.xadj, g.adj
+    src = np.repeat(np.arange(g.num_vertices, dtype=np.int64), np.diff(x))
+    pairs = np.stack([src, a.astype(np.int64)], 1)
+    pairs = pairs[pairs[:, 0] < pairs[:, 1]]
+    m = pairs.shape[0]
+    k = int(round(frac * m))
+    sel = np.zeros(m, bool)
+    sel[np.random.default_rng(seed).choice(m, size=k, replace=False)] = True
+    tr, te = pairs[~sel], pairs[sel]
+    used = np.zeros(g.num_vertices, bool)
+    used[tr.ravel()] = True
+    kept = np.flatnonzero(used)
+    new = np.full(g.num_vertices, -1, np.int64)
+    new[kept] = np.arange(kept.shape[0])
+    t = new[te]
+    t = t[(t >= 0).all(1)]
+    both = np.vstack([new[tr], new[tr][:, ::-1]])
+    key = np.unique(both[:, 0] * kept.shape[0] + both[:, 1])
+    return kept, t, key
+
+
+@pytest.mark.parametrize("scale,samples,frac,seed", [(10, 4000, 0.2, 1), (13, 90000, 0.3, 7),
+                                                     (8, 300, 0.5, 3)])
+def test_device_split_equals_reference_algorithm(cuda, orc, scale, samples, frac, seed):
+    x, a = orc.rmat_graph(scale, samples, 5, densify_ids=True)
+    g = gb.Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
+    sp = gb.split_train_test(g, frac, seed)
+    kept, t, key = _host_split(g, frac, seed)
+    assert np.array_equal(sp.kept_vertices, kept)
+    assert np.array_equal(sp.test_edges, t)
+    tg = sp.train_graph
+    src = np.repeat(np.arange(tg.num_vertices, dtype=np.int64), np.diff(tg.xadj))
+    assert np.array_equal(src * tg.num_vertices + tg.adj, key)
+    assert np.array_equal(g.undirected_pairs(), gb.Graph(len(x) - 1, int(x[-1]), xadj=x,
+                                                         adj=a).undirected_pairs())
+
+
+def test_device_negative_edges_equal_host(cuda, orc):
+    x, a = orc.rmat_graph(11, 30000, 2, densify_ids=True)
+    g = gb.Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
+    g.device_csr()
+    ex = g.undirected_pairs()[::7]
+    for seed in (1, 5):
+        h = gb.sample_negative_edges(g, 5000, seed)
+        d = gb.sample_negative_edges_device(g, 5000, seed)
+        assert np.array_equal(h, d)
+        h = gb.sample_negative_edges(g, 3000, seed, exclude_pairs=ex)
+        d = gb.sample_negative_edges_device(g, 3000, seed, exclude_pairs=ex)
+        assert np.array_equal(h, d)
