@@ -33,9 +33,13 @@
 namespace gb {
 namespace {
 
-constexpr int kFitThreads = 1024;
+constexpr int kFitThreads = 512;  // 16 warps x 128 registers: batched gathers without spills
 constexpr int kFitWarps = kFitThreads / 32;
 constexpr int kMaxK = 16;  // d <= 512
+// rows gathered together per warp: 8 (a 256-row mini-batch = 2 gather
+// rounds per warp) as long as the batch fits the register file
+template <int K>
+constexpr int rows_per_batch() { return K <= 4 ? 8 : (K <= 8 ? 4 : 1); }
 
 __device__ __forceinline__ double sigmoid_clamped(double z) {  // trainer.py:96-99
   z = fmin(fmax(z, -10.0), 10.0);
@@ -91,23 +95,38 @@ __global__ void __launch_bounds__(kFitThreads, 1)
 #pragma unroll
     for (int k = 0; k < K; ++k) g[k] = 0.0;
     double rs = 0.0;
-    for (int r = warp; r < m; r += kFitWarps) {
-      const int64_t row = perm[i0 + r];
-      const float *xr = X + row * d;
-      float x[K];
+    // rows of this warp in batches of kRowsPerBatch: every gather of a batch
+    // is issued before the first dot (the rows are random, so each gather
+    // is a full memory round trip; issuing them together pays it once)
+    constexpr int kRowsPerBatch = rows_per_batch<K>();
+    for (int r0 = warp; r0 < m; r0 += kFitWarps * kRowsPerBatch) {
+      float x[kRowsPerBatch][K];
+      int8_t yv[kRowsPerBatch];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int t = lane + 32 * k;
-        x[k] = t < d ? __ldg(xr + t) : 0.0f;
+      for (int j = 0; j < kRowsPerBatch; ++j) {
+        const int r = r0 + j * kFitWarps;
+        const bool ok = r < m;
+        const int64_t row = ok ? perm[i0 + r] : 0;
+        const float *xr = X + row * d;
+        yv[j] = ok ? y[row] : 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int t = lane + 32 * k;
+          x[j][k] = (ok && t < d) ? __ldg(xr + t) : 0.0f;
+        }
       }
-      double z = 0.0;
 #pragma unroll
-      for (int k = 0; k < K; ++k) z = fma((double)x[k], wl[k], z);
-      z = warp_sum(z) + b;
-      const double resid = sigmoid_clamped(z) - (double)y[row];
+      for (int j = 0; j < kRowsPerBatch; ++j) {
+        if (r0 + j * kFitWarps >= m) break;
+        double z = 0.0;
 #pragma unroll
-      for (int k = 0; k < K; ++k) g[k] = fma((double)x[k], resid, g[k]);
-      rs += resid;
+        for (int k = 0; k < K; ++k) z = fma((double)x[j][k], wl[k], z);
+        z = warp_sum(z) + b;
+        const double resid = sigmoid_clamped(z) - (double)yv[j];
+#pragma unroll
+        for (int k = 0; k < K; ++k) g[k] = fma((double)x[j][k], resid, g[k]);
+        rs += resid;
+      }
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
