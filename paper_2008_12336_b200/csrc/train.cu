@@ -79,6 +79,26 @@ bool pick_variant(int dim, bool aligned, bool exact, Variant &out, bool latency 
   return false;
 }
 
+// The default non-deterministic flags (fast sigmoid, vector-reduction
+// write-back, no reuse) run the HOT instantiations when the layout has them.
+// GB_NO_HOT=1 forces the run-time-flag kernels (A/B measurements).
+bool use_hot(unsigned flags) {
+  static const bool off = [] {
+    const char *e = std::getenv("GB_NO_HOT");
+    return e && std::atoi(e) != 0;
+  }();
+  return !off && !(flags & GB_TRAIN_EXACT) && (flags & GB_TRAIN_FAST_SIGMOID) &&
+         (flags & GB_TRAIN_ATOMIC) && !(flags & GB_TRAIN_REUSE);
+}
+
+void select_hot(Variant &v, unsigned flags, bool diagonal) {
+  if (!use_hot(flags)) return;
+  if (v.pass_hot) v.pass = v.pass_hot;
+  if (v.pass_pipe_hot) v.pass_pipe = v.pass_pipe_hot;
+  PoolFn p = diagonal ? v.pool_hot_diag : v.pool_hot;
+  if (p) v.pool = p;
+}
+
 bool aligned16(const void *p, int dim) {
   return (reinterpret_cast<uintptr_t>(p) & 15u) == 0 && dim % 4 == 0;
 }
@@ -117,6 +137,7 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
   Variant var;
   GB_REQUIRE(pick_variant(dim, aligned16(M, dim), exact, var),
              "gb_train_passes: dim %d unsupported", dim);
+  select_hot(var, flags, false);
   GB_REQUIRE(!sources || n_sources >= 0, "gb_train_passes: bad source list");
   PassArgs a{num_vertices, xadj, adj, sources, n_sources, M, dim, n_neg, seed, rng_stream, pass_begin, n_passes,
              passes_per_epoch, lr_per_epoch, (flags & GB_TRAIN_REUSE) != 0,
@@ -141,12 +162,14 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
     bool pipe = false;
     int occ1 = 0;
     if (groups < full && pick_variant(dim, aligned16(M, dim), exact, lat, true)) {
+      select_hot(lat, flags, false);
       GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
           &occ1, (const void *)lat.pass_pipe, 32, 0));
       pipe = groups <= (int64_t)num_sms() * std::max(occ1, 1) * (32 / lat.G);
     }
     if (const char *env = std::getenv("GB_PIPE")) {
       pipe = std::atoi(env) != 0 && pick_variant(dim, aligned16(M, dim), exact, lat, true);
+      if (pipe) select_hot(lat, flags, false);
       if (pipe)
         GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &occ1, (const void *)lat.pass_pipe, 32, 0));
@@ -181,6 +204,7 @@ GB_API int gb_train_pool_side(float *Msrc, float *Mtgt, int dim, const int32_t *
   Variant var;
   GB_REQUIRE(pick_variant(dim, aligned16(Msrc, dim) && aligned16(Mtgt, dim), exact, var),
              "gb_train_pool_side: dim %d unsupported", dim);
+  select_hot(var, flags, Msrc == Mtgt);
   PoolArgs a{Msrc, Mtgt, dim, targets, n_src, B, lo_t, n_t, n_neg, lr, seed, side, xadj, adj,
              lo_s, pool_side, (flags & GB_TRAIN_REUSE) != 0,
              (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status};

@@ -128,7 +128,9 @@ struct ScalarRow {
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
       const double p = __dmul_rn((double)a.x[k], (double)b.x[k]);
-#pragma unroll
+      // not unrolled: the chain is add-latency bound either way, and the
+      // fully unrolled form made this file the build's long pole
+#pragma unroll 1
       for (int s0 = 0; s0 < 32; s0 += 8) {
         double q[8];
 #pragma unroll
@@ -500,26 +502,26 @@ __device__ __forceinline__ SourceIdx shfl_source(const SourceIdx &d, int k, unsi
 }
 
 // Row half of a source: gather, chained updates, write-back.
-template <class Row, bool EXACT, bool BATCH>
+template <class Row, bool EXACT, bool BATCH, bool HOT>
 __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &g,
                                              const SourceIdx &d, bool &bad, int &first_bad) {
   const int nsamp = 1 + a.n_neg;
+  const bool fast = HOT || a.fast, atomic = HOT || a.atomic, reuse = !HOT && a.reuse;
   const double lr = (double)d.lr;
   Row S;
   S.load(a.M + (int64_t)d.v * a.dim, g.gl, a.dim);
   bool bad_src = false;
   if (EXACT || !BATCH ||
-      !batched_chunk<Row>(S, d.v, d.ids, 1u, a.M, a.dim, lr, a.reuse, g, bad_src, a.fast,
-                          a.atomic))
-    run_chunk<Row, EXACT>(S, d.v, d.ids, 1u, a.M, a.dim, lr, a.reuse, true, false, g, bad_src,
-                          a.fast, a.atomic);
+      !batched_chunk<Row>(S, d.v, d.ids, 1u, a.M, a.dim, lr, reuse, g, bad_src, fast, atomic))
+    run_chunk<Row, EXACT>(S, d.v, d.ids, 1u, a.M, a.dim, lr, reuse, true, false, g, bad_src, fast,
+                          atomic);
   for (int c0 = kChunk; c0 < nsamp; c0 += kChunk) {  // only when n_neg >= kChunk
     int32_t ids[kChunk];
 #pragma unroll
     for (int j = 0; j < kChunk; ++j)
       ids[j] = c0 + j < nsamp ? (int32_t)draw_below(d.key, (uint64_t)(c0 + j), a.V) : -1;
-    run_chunk<Row, EXACT>(S, d.v, ids, 0u, a.M, a.dim, lr, a.reuse, true, false, g, bad_src,
-                          a.fast, a.atomic);
+    run_chunk<Row, EXACT>(S, d.v, ids, 0u, a.M, a.dim, lr, reuse, true, false, g, bad_src, fast,
+                          atomic);
   }
   S.store(a.M + (int64_t)d.v * a.dim, g.gl, a.dim);
   if (bad_src) {
@@ -536,11 +538,15 @@ __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &
 // sources -> xadj -> key -> adj chain and the RNG run once per G sources,
 // G-way parallel, instead of redundantly on every lane for every source.
 // BATCH = true (latency variant, capped launches): batched-dot chunks and one
-// block per SM worth of registers.
-template <class Row, bool EXACT, bool BATCH>
+// block per SM worth of registers.  HOT = true: the default flags (fast
+// sigmoid, vector-reduction write-back, no reuse) fixed at compile time --
+// the runtime-flag branches otherwise triple the unrolled code, and the
+// i-cache misses that cost show up as the top ncu stall (no_instructions).
+template <class Row, bool EXACT, bool BATCH, bool HOT>
 __global__ void __launch_bounds__(kBlock, (BATCH || EXACT) ? 1 : Row::kMinBlocks)
     train_passes_kernel(PassArgs a) {
   constexpr int G = Row::G;
+  const bool fast = HOT || a.fast, atomic = HOT || a.atomic, reuse = !HOT && a.reuse;
   const GroupCtx g = group_ctx<Row>();
   const Slots<Row> sl(a.max_groups);
   if (sl.warp_idle()) return;
@@ -580,8 +586,8 @@ __global__ void __launch_bounds__(kBlock, (BATCH || EXACT) ? 1 : Row::kMinBlocks
             else  // negatives: uniform over V (trainer.py:205-206)
               ids[j] = (int32_t)draw_below(key, (uint64_t)idx, a.V);
           }
-          run_chunk<Row, EXACT>(S, v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, a.reuse, true,
-                                false, g, bad_src, a.fast, a.atomic);
+          run_chunk<Row, EXACT>(S, v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, reuse, true, false,
+                                g, bad_src, fast, atomic);
         }
         S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
         if (bad_src) {
@@ -604,7 +610,7 @@ __global__ void __launch_bounds__(kBlock, (BATCH || EXACT) ? 1 : Row::kMinBlocks
       const int kmax = (int)(total - s0 < G ? total - s0 : G);
       for (int k = 0; k < kmax; ++k) {
         const SourceIdx d = shfl_source(mine, k, g.gmask, G);
-        if (d.active) train_source<Row, EXACT, BATCH>(a, g, d, bad, first_bad);
+        if (d.active) train_source<Row, EXACT, BATCH, HOT>(a, g, d, bad, first_bad);
       }
     }
   }
@@ -655,12 +661,17 @@ __device__ __forceinline__ int64_t lower_bound_adj(const int32_t *__restrict__ a
   return lo;
 }
 
-template <class Row, bool EXACT>
+// MODE 0: flags at run time; 1 / 2: HOT flags (see train_passes_kernel) on
+// an off-diagonal / diagonal pair, so the self-sample branch is compiled out
+// of the off-diagonal kernel.
+template <class Row, bool EXACT, int MODE>
 __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_pool_kernel(PoolArgs a) {
   const GroupCtx g = group_ctx<Row>();
   const Slots<Row> sl(a.max_groups);
   if (sl.warp_idle()) return;
-  const bool diagonal = a.Msrc == a.Mtgt;
+  constexpr bool HOT = MODE != 0;
+  const bool fast = HOT || a.fast, atomic = HOT || a.atomic, reuse = !HOT && a.reuse;
+  const bool diagonal = HOT ? MODE == 2 : a.Msrc == a.Mtgt;
   const int per_t = 1 + a.n_neg;
   const int64_t total = (int64_t)a.B * per_t;
   bool bad = false;
@@ -721,8 +732,8 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
         loaded = true;
       }
       pos_count += __popc(pos_mask);
-      run_chunk<Row, EXACT>(S, i, ids, pos_mask, a.Mtgt, a.dim, a.lr, a.reuse, diagonal, true,
-                            g, bad, a.fast, a.atomic);
+      run_chunk<Row, EXACT>(S, i, ids, pos_mask, a.Mtgt, a.dim, a.lr, reuse, diagonal, true, g,
+                            bad, fast, atomic);
     }
     if (loaded) S.store(a.Msrc + i * (int64_t)a.dim, g.gl, a.dim);
   }
@@ -801,16 +812,27 @@ struct Variant {
   PassFn pass_pipe = nullptr;  // latency (capped launches)
   PoolFn pool = nullptr;
   ListFn lists = nullptr;
+  // HOT instantiations (default flags fixed at compile time); null if absent
+  PassFn pass_hot = nullptr;
+  PassFn pass_pipe_hot = nullptr;
+  PoolFn pool_hot = nullptr;       // off-diagonal pair
+  PoolFn pool_hot_diag = nullptr;  // diagonal pair (Msrc == Mtgt)
 };
 
-template <class Row, bool EXACT>
+template <class Row, bool EXACT, bool WITH_HOT = false>
 Variant make_variant() {
   Variant v;
   v.G = Row::G;
-  v.pass = train_passes_kernel<Row, EXACT, false>;
-  v.pass_pipe = train_passes_kernel<Row, EXACT, true>;
-  v.pool = train_pool_kernel<Row, EXACT>;
+  v.pass = train_passes_kernel<Row, EXACT, false, false>;
+  v.pass_pipe = train_passes_kernel<Row, EXACT, true, false>;
+  v.pool = train_pool_kernel<Row, EXACT, 0>;
   v.lists = apply_lists_kernel<Row, EXACT>;
+  if constexpr (WITH_HOT && !EXACT) {
+    v.pass_hot = train_passes_kernel<Row, false, false, true>;
+    v.pass_pipe_hot = train_passes_kernel<Row, false, true, true>;
+    v.pool_hot = train_pool_kernel<Row, false, 1>;
+    v.pool_hot_diag = train_pool_kernel<Row, false, 2>;
+  }
   return v;
 }
 

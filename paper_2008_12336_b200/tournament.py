@@ -35,6 +35,8 @@ on the GPU.
 """
 from __future__ import annotations
 
+import os
+
 import time
 from dataclasses import dataclass
 from typing import Callable
@@ -152,15 +154,35 @@ def device_pair_fn(g: Graph, cfg: TrainConfig, B: int) -> tuple[PairFn, torch.Te
         _lib.GB_TRAIN_ATOMIC if cfg.atomic_rows and not cfg.deterministic else 0)
     status = _lib.new_status()
     n_s = cfg.negative_samples
+    # GB_POOL_MATERIALIZE=1: draw each side's pool with the thin
+    # gb_fill_pool_side kernel first (one thread per source: the two binary
+    # searches run at full occupancy) and let the pair kernel read the
+    # B targets per source; default: pools drawn inside the pair kernel.
+    # Both give identical pools (tests/test_gpu_parity.py).
+    materialize = os.environ.get("GB_POOL_MATERIALIZE", "0") == "1"
+    pool_buf: list[torch.Tensor] = []
+
+    def targets_for(lo_s: int, hi_s: int, lo_t: int, hi_t: int, seed: int, side: int):
+        if not materialize:
+            return None
+        need = max((hi_s - lo_s) * B, 1)
+        if not pool_buf or pool_buf[0].numel() < need:
+            pool_buf[:] = [torch.empty(need, dtype=torch.int32, device=csr[0].device)]
+        out = pool_buf[0]
+        _lib.call("gb_fill_pool_side", _lib.ptr(csr[0]), _lib.ptr(csr[1]), lo_s, hi_s, lo_t,
+                  hi_t, B, _lib.u64(seed), side, _lib.ptr(out), _lib.stream())
+        return out
 
     def fn(Ma: torch.Tensor, Mb: torch.Tensor, s: PairStep) -> None:
         na, nb = s.hi_a - s.lo_a, s.hi_b - s.lo_b
         if na <= 0 or nb <= 0:
             return
-        _pool_side(Ma, Mb, None, na, B, s.lo_b, nb, n_s, s.lr, s.seed, 2, flags,
+        t = targets_for(s.lo_a, s.hi_a, s.lo_b, s.hi_b, s.seed, 0)
+        _pool_side(Ma, Mb, t, na, B, s.lo_b, nb, n_s, s.lr, s.seed, 2, flags,
                    inflight_cap(cfg, na), status, csr=csr, lo_s=s.lo_a, pool_side=0)
         if s.a != s.b:
-            _pool_side(Mb, Ma, None, nb, B, s.lo_a, na, n_s, s.lr, s.seed, 3, flags,
+            t = targets_for(s.lo_b, s.hi_b, s.lo_a, s.hi_a, s.seed, 1)
+            _pool_side(Mb, Ma, t, nb, B, s.lo_a, na, n_s, s.lr, s.seed, 3, flags,
                        inflight_cap(cfg, nb), status, csr=csr, lo_s=s.lo_b, pool_side=1)
 
     return fn, status
