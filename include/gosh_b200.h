@@ -198,6 +198,30 @@ int gb_train_pool_side(float *Msrc, float *Mtgt, int dim,
                        unsigned flags, int64_t max_groups, int64_t *status,
                        void *stream_handle);
 
+/* Compacted pool side for the pair kernel (same draws as gb_fill_pool_side):
+ * sources v in [lo_s, hi_s) with at least one neighbour in [lo_t, hi_t) get
+ * an entry k < *count: list[k] = v - lo_s, targets[k*B + t] = pool slot t
+ * (global id).  Sources without one train nothing in _train_pool_side
+ * (bigtrain.py:229-231) and are left out.  Entry order is id order within a
+ * warp of 32 sources, warps in any order.  list holds hi_s-lo_s entries,
+ * targets (hi_s-lo_s)*B; count is a device int64 (set by this call). */
+int gb_fill_pool_compact(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
+                         int64_t hi_s, int64_t lo_t, int64_t hi_t, int B,
+                         uint64_t seed, uint64_t side, int32_t *list,
+                         int32_t *targets, int64_t *count, void *stream_handle);
+
+/* _train_pool_side over a compacted pool (gb_fill_pool_compact): entry
+ * k < min(max_src, *count) trains local source list[k] against
+ * targets[k*B ..]; everything else as gb_train_pool_side (negatives keyed by
+ * the source's local id, so results equal the uncompacted launch up to the
+ * order sources run in). */
+int gb_train_pool_list(float *Msrc, float *Mtgt, int dim, const int32_t *list,
+                       const int32_t *targets, const int64_t *count,
+                       int64_t max_src, int B, int64_t lo_t, int64_t n_t,
+                       int n_neg, double lr, uint64_t seed, uint64_t side,
+                       unsigned flags, int64_t max_groups, int64_t *status,
+                       void *stream_handle);
+
 /* Page-lock a caller host buffer in place (cudaHostRegister) so part
  * switches of the partitioned trainer DMA straight from / into the caller's
  * embedding matrix (bigtrain.py:275-299 host staging) without a pinned copy. */

@@ -206,11 +206,40 @@ GB_API int gb_train_pool_side(float *Msrc, float *Mtgt, int dim, const int32_t *
              "gb_train_pool_side: dim %d unsupported", dim);
   select_hot(var, flags, Msrc == Mtgt);
   PoolArgs a{Msrc, Mtgt, dim, targets, n_src, B, lo_t, n_t, n_neg, lr, seed, side, xadj, adj,
-             lo_s, pool_side, (flags & GB_TRAIN_REUSE) != 0,
+             lo_s, pool_side, nullptr, nullptr, (flags & GB_TRAIN_REUSE) != 0,
              (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status};
   int grid = 1;
   if (!exact) {
     int rc = grid_for((const void *)var.pool, var.G, max_groups, n_src, &grid);
+    if (rc) return rc;
+  }
+  var.pool<<<grid, kBlock, 0, as_stream(stream_handle)>>>(a);
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
+GB_API int gb_train_pool_list(float *Msrc, float *Mtgt, int dim, const int32_t *list,
+                              const int32_t *targets, const int64_t *count, int64_t max_src,
+                              int B, int64_t lo_t, int64_t n_t, int n_neg, double lr,
+                              uint64_t seed, uint64_t side, unsigned flags, int64_t max_groups,
+                              int64_t *status, void *stream_handle) {
+  GB_REQUIRE(dim >= 1 && B >= 1 && n_neg >= 0 && max_src >= 0 && n_t >= 0,
+             "gb_train_pool_list: bad sizes");
+  GB_REQUIRE(Msrc && Mtgt && status && list && targets && count,
+             "gb_train_pool_list: null pointer");
+  if (max_src == 0 || n_t == 0) return GB_OK;
+  const bool exact = flags & GB_TRAIN_EXACT;
+  Variant var;
+  GB_REQUIRE(pick_variant(dim, aligned16(Msrc, dim) && aligned16(Mtgt, dim), exact, var),
+             "gb_train_pool_list: dim %d unsupported", dim);
+  select_hot(var, flags, Msrc == Mtgt);
+  PoolArgs a{Msrc, Mtgt, dim, targets, max_src, B, lo_t, n_t, n_neg, lr, seed, side, nullptr,
+             nullptr, 0, 0, list, count, (flags & GB_TRAIN_REUSE) != 0,
+             (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0,
+             exact ? 1 : max_groups, status};
+  int grid = 1;
+  if (!exact) {
+    int rc = grid_for((const void *)var.pool, var.G, max_groups, max_src, &grid);
     if (rc) return rc;
   }
   var.pool<<<grid, kBlock, 0, as_stream(stream_handle)>>>(a);
@@ -271,9 +300,63 @@ __global__ void fill_pool_kernel(const int64_t *__restrict__ xadj, const int32_t
       row[t] = cnt > 0 ? adj[first + draw_below(key, (uint64_t)t, cnt)] : -1;
   }
 }
+
+// Compacted pool side: the same draws as fill_pool_kernel, but only sources
+// with a neighbour in [lo_t, hi_t) get an entry (list[k] = v - lo_s, pool
+// row targets[k*B ..]); warp-aggregated append, so entries of one warp stay
+// in id order while warps land in any order (Hogwild launches do not depend
+// on source order).  Sources without such a neighbour train nothing
+// (bigtrain.py:229-231), so the pair kernel never sees them.
+__global__ void fill_pool_compact_kernel(const int64_t *__restrict__ xadj,
+                                         const int32_t *__restrict__ adj, int64_t lo_s,
+                                         int64_t hi_s, int64_t lo_t, int64_t hi_t, int B,
+                                         uint64_t seed, uint64_t side, int32_t *__restrict__ list,
+                                         int32_t *__restrict__ targets,
+                                         unsigned long long *count) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t v0 = lo_s + (int64_t)blockIdx.x * blockDim.x; v0 < hi_s;
+       v0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = v0 + threadIdx.x;
+    int64_t first = 0, cnt = 0;
+    if (v < hi_s) {
+      const int64_t e1 = __ldg(xadj + v + 1);
+      first = lower_bound_adj(adj, __ldg(xadj + v), e1, lo_t);
+      cnt = lower_bound_adj(adj, first, e1, hi_t) - first;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, cnt > 0);
+    if (m == 0) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(count, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (cnt > 0) {
+      const int64_t slot = (int64_t)base + __popc(m & ((1u << lane) - 1u));
+      list[slot] = (int32_t)(v - lo_s);
+      const uint64_t key = stream_key(seed, side, 0, (uint64_t)v);
+      int32_t *row = targets + slot * B;
+      for (int t = 0; t < B; ++t) row[t] = __ldg(adj + first + draw_below(key, (uint64_t)t, cnt));
+    }
+  }
+}
 }  // namespace
 }  // namespace tk
 }  // namespace gb
+
+GB_API int gb_fill_pool_compact(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
+                                int64_t hi_s, int64_t lo_t, int64_t hi_t, int B, uint64_t seed,
+                                uint64_t side, int32_t *list, int32_t *targets, int64_t *count,
+                                void *stream_handle) {
+  GB_REQUIRE(xadj && adj && list && targets && count && B >= 1 && hi_s >= lo_s && hi_t >= lo_t,
+             "gb_fill_pool_compact: bad args");
+  GB_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int64_t), as_stream(stream_handle)));
+  const int64_t n = hi_s - lo_s;
+  if (n == 0) return GB_OK;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+  gb::tk::fill_pool_compact_kernel<<<(int)blocks, 256, 0, as_stream(stream_handle)>>>(
+      xadj, adj, lo_s, hi_s, lo_t, hi_t, B, seed, side, list, targets,
+      reinterpret_cast<unsigned long long *>(count));
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
 
 GB_API int gb_fill_pool_side(const int64_t *xadj, const int32_t *adj, int64_t lo_s, int64_t hi_s,
                              int64_t lo_t, int64_t hi_t, int B, uint64_t seed, uint64_t side,

@@ -297,6 +297,15 @@ __device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t
   for (int j = 0; j < kChunk; ++j)
     if (ids[j] >= 0 && !(self_possible && ids[j] == src_row))
       R[j].load(Mtgt + (int64_t)ids[j] * dim, g.gl, dim);
+  // Repeated ids are rare (~C(4,2)/n per chunk): the row forwarding runs
+  // behind one branch per chunk instead of as predicated copies on every
+  // update (those cost ~10% of the pair kernel's instructions).
+  bool dup = false;
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j)
+#pragma unroll
+    for (int jj = j + 1; jj < kChunk; ++jj)
+      if (ids[j] >= 0 && ids[j] == ids[jj]) dup = true;
 #pragma unroll
   for (int j = 0; j < kChunk; ++j) {
     const int32_t s = ids[j];
@@ -312,9 +321,11 @@ __device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t
     float sc = nce_score(acc, b, lr, bad, fast && !EXACT);
     update_pair_writeback(S, R[j], sc, reuse, atomic && !EXACT, Mtgt + (int64_t)s * dim, g.gl,
                           dim);
+    if (dup) {
 #pragma unroll
-    for (int jj = j + 1; jj < kChunk; ++jj)
-      if (ids[jj] == s) R[jj] = R[j];
+      for (int jj = j + 1; jj < kChunk; ++jj)
+        if (ids[jj] == s) R[jj] = R[j];
+    }
   }
 }
 
@@ -641,6 +652,11 @@ struct PoolArgs {
   const int32_t *__restrict__ adj;
   int64_t lo_s;
   uint64_t pool_side;
+  // compacted sources (gb_fill_pool_compact): source k of the launch is
+  // src_list[k] (local id), its pool row is targets[k*B ..], and only the
+  // first min(n_src, *n_list) entries are live.  Null: source k is k.
+  const int32_t *__restrict__ src_list;
+  const int64_t *__restrict__ n_list;
   bool reuse;
   bool fast;
   bool atomic;
@@ -664,8 +680,16 @@ __device__ __forceinline__ int64_t lower_bound_adj(const int32_t *__restrict__ a
 // MODE 0: flags at run time; 1 / 2: HOT flags (see train_passes_kernel) on
 // an off-diagonal / diagonal pair, so the self-sample branch is compiled out
 // of the off-diagonal kernel.
+//
+// Sample ids come in windows of kWin = 2 chunks: lane l of the group draws
+// flat samples l, l + G, ... of the window (the positive from the pool or the
+// CSR, a negative from the counter-based key), and the chunks take them by
+// shuffle -- the RNG runs once per sample instead of once per lane.
 template <class Row, bool EXACT, int MODE>
 __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_pool_kernel(PoolArgs a) {
+  constexpr int G = Row::G;
+  constexpr int kWin = 2 * kChunk;
+  constexpr int PL = (kWin + G - 1) / G;  // window samples per lane
   const GroupCtx g = group_ctx<Row>();
   const Slots<Row> sl(a.max_groups);
   if (sl.warp_idle()) return;
@@ -673,17 +697,21 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
   const bool fast = HOT || a.fast, atomic = HOT || a.atomic, reuse = !HOT && a.reuse;
   const bool diagonal = HOT ? MODE == 2 : a.Msrc == a.Mtgt;
   const int per_t = 1 + a.n_neg;
-  const int64_t total = (int64_t)a.B * per_t;
+  const int total = a.B * per_t;
+  const int gbase = (int)(threadIdx.x & 31) - g.gl;
+  const int64_t n = a.src_list ? min(a.n_src, *a.n_list) : a.n_src;
   bool bad = false;
   unsigned long long pos_count = 0;
 
-  for (int64_t base = sl.warp_base; base < a.n_src; base += sl.eff) {
-    const int64_t i = base + (sl.gid - sl.warp_base);
-    if (!sl.enabled || i >= a.n_src) continue;
+  for (int64_t base = sl.warp_base; base < n; base += sl.eff) {
+    const int64_t k = base + (sl.gid - sl.warp_base);
+    if (!sl.enabled || k >= n) continue;
+    const int64_t i = a.src_list ? (int64_t)__ldg(a.src_list + k) : k;
+    const int32_t *trow = a.targets ? a.targets + k * a.B : nullptr;
     // pool side of this source: either the materialized row or the fused draw
     int64_t first = 0, cnt = 0;
     uint64_t pkey = 0;
-    if (a.targets == nullptr) {
+    if (trow == nullptr) {
       const int64_t v = a.lo_s + i;
       const int64_t e0 = __ldg(a.xadj + v), e1 = __ldg(a.xadj + v + 1);
       first = lower_bound_adj(a.adj, e0, e1, a.lo_t);
@@ -694,46 +722,57 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
     const uint64_t key = stream_key(a.seed, a.side, 1, (uint64_t)i);
     Row S;
     bool loaded = false;
-    // (slot t, sample q) of flat index c0 + j, advanced incrementally (no
-    // 64-bit division per sample)
-    int64_t t_cur = 0;
-    int q_cur = 0;
-    for (int64_t c0 = 0; c0 < total; c0 += kChunk) {
-      int32_t ids[kChunk];
-      unsigned pos_mask = 0;
+    for (int c0 = 0; c0 < total; c0 += kWin) {
+      int32_t mine[PL];
+      unsigned wpos = 0;  // bit w: window sample w is a live positive
 #pragma unroll
-      for (int j = 0; j < kChunk; ++j) {
-        const int64_t t = t_cur;
-        const int q = q_cur;
-        if (++q_cur == per_t) {
-          q_cur = 0;
-          ++t_cur;
-        }
-        ids[j] = -1;
-        if (c0 + j >= total) continue;
-        if (a.targets != nullptr) {
-          const int64_t tgt = __ldg(a.targets + i * a.B + t);
-          if (tgt < 0) continue;  // absent slot: no positive, no negatives
-          if (q == 0) {
-            ids[j] = (int32_t)(tgt - a.lo_t);
-            pos_mask |= 1u << j;
-            continue;
+      for (int p = 0; p < PL; ++p) {
+        const int w = g.gl + p * G;
+        const int f = c0 + w;
+        int32_t id = -1;
+        bool pos = false;
+        if (w < kWin && f < total) {
+          const int t = f / per_t, q = f - t * per_t;
+          if (trow != nullptr) {
+            const int32_t tgt = __ldg(trow + t);
+            if (tgt >= 0) {  // absent slot: no positive, no negatives
+              if (q == 0) {
+                id = (int32_t)(tgt - a.lo_t);
+                pos = true;
+              } else {
+                id = (int32_t)draw_below(key, (uint64_t)(t * a.n_neg + (q - 1)), a.n_t);
+              }
+            }
+          } else if (q == 0) {  // fused pool: cnt > 0, so no slot is absent
+            id = (int32_t)(__ldg(a.adj + first + draw_below(pkey, (uint64_t)t, cnt)) - a.lo_t);
+            pos = true;
+          } else {
+            id = (int32_t)draw_below(key, (uint64_t)(t * a.n_neg + (q - 1)), a.n_t);
           }
-        } else if (q == 0) {  // fused pool: cnt > 0, so no slot is absent
-          ids[j] = (int32_t)(__ldg(a.adj + first + draw_below(pkey, (uint64_t)t, cnt)) - a.lo_t);
-          pos_mask |= 1u << j;
-          continue;
         }
-        ids[j] = (int32_t)draw_below(key, (uint64_t)(t * a.n_neg + (q - 1)), a.n_t);
+        mine[p] = id;
+        unsigned b = __ballot_sync(g.gmask, pos);
+        if (G < 32) b = (b >> gbase) & ((1u << (G < 32 ? G : 0)) - 1u);
+        wpos |= b << (p * G);
       }
-      if (!(ids[0] >= 0 || ids[1] >= 0 || ids[2] >= 0 || ids[3] >= 0)) continue;
-      if (!loaded) {
-        S.load(a.Msrc + i * (int64_t)a.dim, g.gl, a.dim);
-        loaded = true;
+      int32_t win[kWin];
+#pragma unroll
+      for (int w = 0; w < kWin; ++w) win[w] = __shfl_sync(g.gmask, mine[w / G], w % G, G);
+#pragma unroll 1
+      for (int h = 0; h < kWin / kChunk; ++h) {  // not unrolled: one copy of the chunk code
+        int32_t ids[kChunk];
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) ids[j] = h ? win[kChunk + j] : win[j];
+        if (!(ids[0] >= 0 || ids[1] >= 0 || ids[2] >= 0 || ids[3] >= 0)) continue;
+        if (!loaded) {
+          S.load(a.Msrc + i * (int64_t)a.dim, g.gl, a.dim);
+          loaded = true;
+        }
+        const unsigned pos_mask = (wpos >> (h * kChunk)) & ((1u << kChunk) - 1u);
+        pos_count += __popc(pos_mask);
+        run_chunk<Row, EXACT>(S, i, ids, pos_mask, a.Mtgt, a.dim, a.lr, reuse, diagonal, true, g,
+                              bad, fast, atomic);
       }
-      pos_count += __popc(pos_mask);
-      run_chunk<Row, EXACT>(S, i, ids, pos_mask, a.Mtgt, a.dim, a.lr, reuse, diagonal, true, g,
-                            bad, fast, atomic);
     }
     if (loaded) S.store(a.Msrc + i * (int64_t)a.dim, g.gl, a.dim);
   }

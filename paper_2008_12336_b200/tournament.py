@@ -20,8 +20,8 @@ module schedules that:
     the arrangement is back at the start;
   * a pair (a,b), a>=b as in rotation_pairs, trains side 2 (sources of a
     against b) then side 3 exactly like train_large's pair step, with the
-    positive pools drawn in-kernel from the replicated device CSR
-    (gb_train_pool_side, targets=NULL) and seed _derived_seed(seed, stream,
+    positive pools drawn on the GPU from the replicated device CSR
+    (bigtrain.PairSides: compacted pools + list pair kernel) and seed _derived_seed(seed, stream,
     rot*P + index of (a,b) in rotation_pairs(K)) -- the pair's seed does
     not depend on the number of GPUs;
   * lr decays per rotation (bigtrain.py:432) and the rotation count is
@@ -45,10 +45,10 @@ import numpy as np
 import torch
 
 from . import _lib
-from .bigtrain import PartitionPlan, _derived_seed, _pool_side, rotation_pairs
+from .bigtrain import PairSides, PartitionPlan, _derived_seed, rotation_pairs
 from .errors import ConfigError
 from .graph import Graph
-from .trainer import TrainConfig, inflight_cap, lr_at
+from .trainer import TrainConfig, lr_at
 
 TOP, BOT = 0, 1
 
@@ -145,8 +145,9 @@ PairFn = Callable[[torch.Tensor, torch.Tensor, PairStep], None]
 
 
 def device_pair_fn(g: Graph, cfg: TrainConfig, B: int) -> tuple[PairFn, torch.Tensor]:
-    """Pair step on the GPU: gb_train_pool_side with in-kernel pools, side 2
-    then side 3 (bigtrain.py:241-260); returns (fn, status block)."""
+    """Pair step on the GPU: side 2 then side 3 (bigtrain.py:241-260) through
+    bigtrain.PairSides (compacted pools + list pair kernel by default);
+    returns (fn, status block)."""
     _lib.require_cuda()
     csr = g.device_csr()
     flags = (_lib.GB_TRAIN_REUSE if cfg.reuse_updated_source else 0) | (
@@ -154,36 +155,14 @@ def device_pair_fn(g: Graph, cfg: TrainConfig, B: int) -> tuple[PairFn, torch.Te
         _lib.GB_TRAIN_ATOMIC if cfg.atomic_rows and not cfg.deterministic else 0)
     status = _lib.new_status()
     n_s = cfg.negative_samples
-    # GB_POOL_MATERIALIZE=1: draw each side's pool with the thin
-    # gb_fill_pool_side kernel first (one thread per source: the two binary
-    # searches run at full occupancy) and let the pair kernel read the
-    # B targets per source; default: pools drawn inside the pair kernel.
-    # Both give identical pools (tests/test_gpu_parity.py).
-    materialize = os.environ.get("GB_POOL_MATERIALIZE", "0") == "1"
-    pool_buf: list[torch.Tensor] = []
-
-    def targets_for(lo_s: int, hi_s: int, lo_t: int, hi_t: int, seed: int, side: int):
-        if not materialize:
-            return None
-        need = max((hi_s - lo_s) * B, 1)
-        if not pool_buf or pool_buf[0].numel() < need:
-            pool_buf[:] = [torch.empty(need, dtype=torch.int32, device=csr[0].device)]
-        out = pool_buf[0]
-        _lib.call("gb_fill_pool_side", _lib.ptr(csr[0]), _lib.ptr(csr[1]), lo_s, hi_s, lo_t,
-                  hi_t, B, _lib.u64(seed), side, _lib.ptr(out), _lib.stream())
-        return out
+    side_step = PairSides(csr, cfg, flags, B, status)
 
     def fn(Ma: torch.Tensor, Mb: torch.Tensor, s: PairStep) -> None:
-        na, nb = s.hi_a - s.lo_a, s.hi_b - s.lo_b
-        if na <= 0 or nb <= 0:
+        if s.hi_a - s.lo_a <= 0 or s.hi_b - s.lo_b <= 0:
             return
-        t = targets_for(s.lo_a, s.hi_a, s.lo_b, s.hi_b, s.seed, 0)
-        _pool_side(Ma, Mb, t, na, B, s.lo_b, nb, n_s, s.lr, s.seed, 2, flags,
-                   inflight_cap(cfg, na), status, csr=csr, lo_s=s.lo_a, pool_side=0)
+        side_step(Ma, Mb, s.lo_a, s.hi_a, s.lo_b, s.hi_b, s.seed, s.lr, 0, 2)
         if s.a != s.b:
-            t = targets_for(s.lo_b, s.hi_b, s.lo_a, s.hi_a, s.seed, 1)
-            _pool_side(Mb, Ma, t, nb, B, s.lo_a, na, n_s, s.lr, s.seed, 3, flags,
-                       inflight_cap(cfg, nb), status, csr=csr, lo_s=s.lo_b, pool_side=1)
+            side_step(Mb, Ma, s.lo_b, s.hi_b, s.lo_a, s.hi_a, s.seed, s.lr, 1, 3)
 
     return fn, status
 

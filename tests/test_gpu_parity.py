@@ -393,6 +393,117 @@ def test_fused_pool_equals_materialized(cuda, orc):
     assert int(st[2]) == want_pos
 
 
+def _compact_pool(G, lo_s, hi_s, lo_t, hi_t, B, seed, side, sort=True):
+    xa, aa = G.device_csr()
+    n = hi_s - lo_s
+    lst = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    tg = torch.empty(max(n * B, 1), dtype=torch.int32, device="cuda")
+    cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+    _lib.call("gb_fill_pool_compact", _lib.ptr(xa), _lib.ptr(aa), lo_s, hi_s, lo_t, hi_t, B,
+              _lib.u64(seed), side, _lib.ptr(lst), _lib.ptr(tg), _lib.ptr(cnt), _lib.stream())
+    c = int(cnt.item())
+    lst_h = lst[:c].cpu().numpy()
+    tg_h = tg[: c * B].cpu().numpy().reshape(c, B)
+    if sort:
+        o = np.argsort(lst_h, kind="stable")
+        lst_h, tg_h = lst_h[o], tg_h[o]
+    return lst_h, tg_h
+
+
+def test_compact_pool_equals_materialized(cuda, orc):
+    """gb_fill_pool_compact keeps exactly the sources with a pool and their
+    materialized rows; the list-driven pair kernel (serial, EXACT) then equals
+    the oracle's _train_pool_side bit for bit."""
+    x, a = orc.rmat_graph(12, 40000, 9, densify_ids=True)
+    G = Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
+    n = G.num_vertices
+    lo_j, hi_j, lo_k, hi_k = 0, n // 3, n // 3, 2 * n // 3
+    B, n_neg, lr, seed = 5, 3, 0.05, 77
+    tj = orc.fill_pool_side(x, a, lo_j, hi_j, lo_k, hi_k, B, seed, 0)
+    lst, tg = _compact_pool(G, lo_j, hi_j, lo_k, hi_k, B, seed, 0)
+    live = np.flatnonzero(tj[:, 0] >= 0)
+    assert np.array_equal(lst, live) and np.array_equal(tg, tj[live])
+    assert 0 < len(live) < hi_j - lo_j
+    M0 = orc.init_embedding(n, 32, 4)
+    Mj, Mk = M0[lo_j:hi_j].copy(), M0[lo_k:hi_k].copy()
+    want_pos = orc.train_pool_side(Mj, Mk, tj, lo_k, hi_k - lo_k, n_neg, lr, seed, 2)
+    dj = torch.from_numpy(M0[lo_j:hi_j].copy()).cuda()
+    dk = torch.from_numpy(M0[lo_k:hi_k].copy()).cuda()
+    dl = torch.from_numpy(lst.astype(np.int32)).cuda()
+    dt = torch.from_numpy(np.ascontiguousarray(tg, dtype=np.int32)).cuda()
+    dc = torch.tensor([len(lst)], dtype=torch.int64, device="cuda")
+    st = _lib.new_status()
+    _lib.call("gb_train_pool_list", _lib.ptr(dj), _lib.ptr(dk), 32, _lib.ptr(dl), _lib.ptr(dt),
+              _lib.ptr(dc), hi_j - lo_j, B, lo_k, hi_k - lo_k, n_neg, lr, seed, 2,
+              _lib.GB_TRAIN_EXACT, 1, _lib.ptr(st), _lib.stream())
+    assert np.array_equal(dj.cpu().numpy(), Mj) and np.array_equal(dk.cpu().numpy(), Mk)
+    assert int(st[2]) == want_pos
+
+
+@pytest.mark.parametrize("dim", [16, 128, 256])
+@pytest.mark.parametrize("diagonal", [False, True])
+def test_pair_kernel_fast_path_serial(cuda, orc, dim, diagonal):
+    """The default (HOT) pair kernels -- fused pools and compacted lists --
+    run serially (one group) against the oracle: tree dot + fp32 sigmoid
+    within the 1e-5 bar, positives counted exactly.  Diagonal pairs on a
+    small part exercise self-samples (load-once rule)."""
+    x, a = orc.rmat_graph(10, 12000, 3, densify_ids=True)
+    G = Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
+    n = G.num_vertices
+    if diagonal:
+        lo_j, hi_j = 0, 96
+        lo_k, hi_k = lo_j, hi_j
+    else:
+        lo_j, hi_j, lo_k, hi_k = 0, n // 2, n // 2, n
+    B, n_neg, lr, seed = 5, 3, 0.05, 31
+    flags = _lib.GB_TRAIN_FAST_SIGMOID | _lib.GB_TRAIN_ATOMIC
+    tj = orc.fill_pool_side(x, a, lo_j, hi_j, lo_k, hi_k, B, seed, 0)
+    M0 = orc.init_embedding(n, dim, 4) * np.float32(40.0)  # |dot| ~ 1: sigmoid off its tails
+    Mj = M0[lo_j:hi_j].copy()
+    Mk = Mj if diagonal else M0[lo_k:hi_k].copy()
+    want_pos = orc.train_pool_side(Mj, Mk, tj, lo_k, hi_k - lo_k, n_neg, lr, seed, 2)
+    xa, aa = G.device_csr()
+    for mode in ("fused", "list"):
+        dj = torch.from_numpy(M0[lo_j:hi_j].copy()).cuda()
+        dk = dj if diagonal else torch.from_numpy(M0[lo_k:hi_k].copy()).cuda()
+        st = _lib.new_status()
+        if mode == "fused":
+            _lib.call("gb_train_pool_side", _lib.ptr(dj), _lib.ptr(dk), dim, None, hi_j - lo_j, B,
+                      lo_k, hi_k - lo_k, n_neg, lr, seed, 2, _lib.ptr(xa), _lib.ptr(aa), lo_j, 0,
+                      flags, 1, _lib.ptr(st), _lib.stream())
+        else:
+            lst, tg = _compact_pool(G, lo_j, hi_j, lo_k, hi_k, B, seed, 0)
+            dl = torch.from_numpy(lst.astype(np.int32)).cuda()
+            dt = torch.from_numpy(np.ascontiguousarray(tg, dtype=np.int32)).cuda()
+            dc = torch.tensor([len(lst)], dtype=torch.int64, device="cuda")
+            _lib.call("gb_train_pool_list", _lib.ptr(dj), _lib.ptr(dk), dim, _lib.ptr(dl),
+                      _lib.ptr(dt), _lib.ptr(dc), hi_j - lo_j, B, lo_k, hi_k - lo_k, n_neg, lr,
+                      seed, 2, flags, 1, _lib.ptr(st), _lib.stream())
+        assert int(st[2]) == want_pos, mode
+        assert _rel_err(dj.cpu().numpy(), Mj) <= REL_TOL, mode
+        if not diagonal:
+            assert _rel_err(dk.cpu().numpy(), Mk) <= REL_TOL, mode
+
+
+def test_tournament_pool_modes_agree(cuda, monkeypatch):
+    """The three pool modes of the tournament draw the same pools: the same
+    positive count, and (serial, one group per launch) the same embedding up
+    to the Hogwild kernels' summation order."""
+    from paper_2008_12336_b200 import tournament as tn
+    G = gb.rmat_graph(11, 20000, 5, densify_ids=True)
+    cfg = gb.TrainConfig(dim=32, seed=3, negative_samples=3, max_inflight=1)
+    outs = {}
+    for mode in ("fused", "materialize", "compact"):
+        monkeypatch.setenv("GB_POOL_MODE", mode)
+        M = torch.from_numpy(gb.init_embedding(G.num_vertices, 32, 3)).cuda()
+        st = tn.train_tournament(G, M, cfg, 2, batch_size=5, num_ranks=2)
+        outs[mode] = (st["pos_updates"], M.cpu().numpy())
+    assert outs["fused"][0] == outs["materialize"][0] == outs["compact"][0] > 0
+    assert np.array_equal(outs["fused"][1], outs["materialize"][1])
+    # compaction changes the order sources run in, not the samples
+    assert _rel_err(outs["compact"][1], outs["fused"][1]) < 0.05
+
+
 def test_train_large_deterministic_bit_exact(cuda, golden):
     g = golden("large.npz")
     G = _graphs(g)[0]
