@@ -331,9 +331,11 @@ def run_tournament(args):
                          atomic_rows=(not args.store_rows))
     M = torch.from_numpy(gb.init_embedding(V, DIM, 1)).to(dev)
 
+    vr = max(1, args.virtual_ranks)
+
     def step():
         return tn.train_tournament(G, M, cfg, 1, batch_size=B, gather=False,
-                                   num_ranks=None if world > 1 else 1)
+                                   num_ranks=None if world > 1 else vr)
 
     for _ in range(args.warmup):
         step()
@@ -360,7 +362,7 @@ def run_tournament(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     value = upd / (total_ms / 1000.0)  # pos_updates are already summed over ranks
-    K = 2 * world
+    K = 2 * world if world > 1 else 2 * vr
     bpu = 8 * DIM + (8 * DIM) / (B * (1 + NNEG))
     peak, peak_src = measured_peak()
     line = {
@@ -371,7 +373,9 @@ def run_tournament(args):
         "config": workload_config({
             "workload": f"part-pair tournament on the C2 graph, K={K} parts, B={B}, d={DIM}",
             "step": "one rotation: K(K+1)/2 pairs, K-1 part exchanges",
-            "parallelism": f"tournament over {world} GPU(s)", "vertices": V}),
+            "parallelism": f"tournament over {world} GPU(s)"
+                           + (f" ({vr} virtual ranks)" if world == 1 and vr > 1 else ""),
+            "vertices": V, "pool_mode": os.environ.get("GB_POOL_MODE", "compact")}),
         "roofline": {"bound": "hbm", "achieved": value * bpu / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": value * bpu / 1e9 / world / peak, "traffic": None,
                      "bytes_per_update": bpu, "peak_source": peak_src,
@@ -393,6 +397,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", choices=["c2", "tournament"], default="c2")
+    ap.add_argument("--virtual-ranks", type=int, default=1,
+                    help="tournament on one GPU: run the schedule of R ranks (K = 2R parts) "
+                         "in this process")
     ap.add_argument("--store-rows", action="store_true",
                     help="write sample rows back with plain stores instead of the default "
                          "vector reductions (GB_TRAIN_ATOMIC off)")

@@ -91,12 +91,19 @@ bool use_hot(unsigned flags) {
          (flags & GB_TRAIN_ATOMIC) && !(flags & GB_TRAIN_REUSE);
 }
 
-void select_hot(Variant &v, unsigned flags, bool diagonal) {
+void select_hot(Variant &v, unsigned flags, bool diagonal, bool pool_materialized = true) {
   if (!use_hot(flags)) return;
-  if (v.pass_hot) v.pass = v.pass_hot;
+  static const bool fetch = [] {
+    const char *e = std::getenv("GB_PASS_FETCH");
+    return e && std::atoi(e) != 0;
+  }();
+  if (fetch && v.pass_fetch_hot)
+    v.pass = v.pass_fetch_hot;
+  else if (v.pass_hot)
+    v.pass = v.pass_hot;
   if (v.pass_pipe_hot) v.pass_pipe = v.pass_pipe_hot;
   PoolFn p = diagonal ? v.pool_hot_diag : v.pool_hot;
-  if (p) v.pool = p;
+  if (p && pool_materialized) v.pool = p;
 }
 
 bool aligned16(const void *p, int dim) {
@@ -204,7 +211,7 @@ GB_API int gb_train_pool_side(float *Msrc, float *Mtgt, int dim, const int32_t *
   Variant var;
   GB_REQUIRE(pick_variant(dim, aligned16(Msrc, dim) && aligned16(Mtgt, dim), exact, var),
              "gb_train_pool_side: dim %d unsupported", dim);
-  select_hot(var, flags, Msrc == Mtgt);
+  select_hot(var, flags, Msrc == Mtgt, targets != nullptr);
   PoolArgs a{Msrc, Mtgt, dim, targets, n_src, B, lo_t, n_t, n_neg, lr, seed, side, xadj, adj,
              lo_s, pool_side, nullptr, nullptr, (flags & GB_TRAIN_REUSE) != 0,
              (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status};

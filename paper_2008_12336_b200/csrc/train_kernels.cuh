@@ -522,17 +522,22 @@ __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &
   Row S;
   S.load(a.M + (int64_t)d.v * a.dim, g.gl, a.dim);
   bool bad_src = false;
-  if (EXACT || !BATCH ||
-      !batched_chunk<Row>(S, d.v, d.ids, 1u, a.M, a.dim, lr, reuse, g, bad_src, fast, atomic))
-    run_chunk<Row, EXACT>(S, d.v, d.ids, 1u, a.M, a.dim, lr, reuse, true, false, g, bad_src, fast,
-                          atomic);
-  for (int c0 = kChunk; c0 < nsamp; c0 += kChunk) {  // only when n_neg >= kChunk
+  if constexpr (BATCH) {
+    if (EXACT ||
+        !batched_chunk<Row>(S, d.v, d.ids, 1u, a.M, a.dim, lr, reuse, g, bad_src, fast, atomic))
+      run_chunk<Row, EXACT>(S, d.v, d.ids, 1u, a.M, a.dim, lr, reuse, true, false, g, bad_src,
+                            fast, atomic);
+  }
+  // one run_chunk call site for the non-batched form (code size / registers)
+  for (int c0 = BATCH ? kChunk : 0; c0 < nsamp; c0 += kChunk) {
     int32_t ids[kChunk];
 #pragma unroll
     for (int j = 0; j < kChunk; ++j)
-      ids[j] = c0 + j < nsamp ? (int32_t)draw_below(d.key, (uint64_t)(c0 + j), a.V) : -1;
-    run_chunk<Row, EXACT>(S, d.v, ids, 0u, a.M, a.dim, lr, reuse, true, false, g, bad_src, fast,
-                          atomic);
+      ids[j] = c0 == 0 ? d.ids[j]
+                       : (c0 + j < nsamp ? (int32_t)draw_below(d.key, (uint64_t)(c0 + j), a.V)
+                                         : -1);
+    run_chunk<Row, EXACT>(S, d.v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, reuse, true, false, g,
+                          bad_src, fast, atomic);
   }
   S.store(a.M + (int64_t)d.v * a.dim, g.gl, a.dim);
   if (bad_src) {
@@ -548,15 +553,18 @@ __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &
 // group trains the G sources one by one from shuffled indices -- the
 // sources -> xadj -> key -> adj chain and the RNG run once per G sources,
 // G-way parallel, instead of redundantly on every lane for every source.
-// BATCH = true (latency variant, capped launches): batched-dot chunks and one
-// block per SM worth of registers.  HOT = true: the default flags (fast
+// KIND 0: throughput variant (index chain inline per source); 1: latency
+// variant (capped launches): batched index fetch, batched-dot chunks and one
+// block per SM worth of registers; 2: throughput variant with the batched
+// index fetch (sequential dots, full occupancy).  HOT = true: the default flags (fast
 // sigmoid, vector-reduction write-back, no reuse) fixed at compile time --
 // the runtime-flag branches otherwise triple the unrolled code, and the
 // i-cache misses that cost show up as the top ncu stall (no_instructions).
-template <class Row, bool EXACT, bool BATCH, bool HOT>
-__global__ void __launch_bounds__(kBlock, (BATCH || EXACT) ? 1 : Row::kMinBlocks)
+template <class Row, bool EXACT, int KIND, bool HOT>
+__global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : Row::kMinBlocks)
     train_passes_kernel(PassArgs a) {
   constexpr int G = Row::G;
+  constexpr bool BATCH = KIND == 1;
   const bool fast = HOT || a.fast, atomic = HOT || a.atomic, reuse = !HOT && a.reuse;
   const GroupCtx g = group_ctx<Row>();
   const Slots<Row> sl(a.max_groups);
@@ -566,7 +574,7 @@ __global__ void __launch_bounds__(kBlock, (BATCH || EXACT) ? 1 : Row::kMinBlocks
   const int64_t n = a.sources ? a.n_sources : a.V;
   if (sl.warp_base >= n) return;
   const int64_t lane_off = sl.gid - sl.warp_base;
-  if constexpr (!BATCH) {
+  if constexpr (KIND == 0) {
     // throughput variant (full occupancy, HBM-bound): the index chain is
     // computed inline per source -- its latency hides behind other warps and
     // this keeps the kernel within 128 registers (2 blocks per SM)
@@ -619,6 +627,7 @@ __global__ void __launch_bounds__(kBlock, (BATCH || EXACT) ? 1 : Row::kMinBlocks
         fetch_source(a, a.pass_begin + q, i, s < total && sl.enabled && i < n, mine);
       }
       const int kmax = (int)(total - s0 < G ? total - s0 : G);
+#pragma unroll 1
       for (int k = 0; k < kmax; ++k) {
         const SourceIdx d = shfl_source(mine, k, g.gmask, G);
         if (d.active) train_source<Row, EXACT, BATCH, HOT>(a, g, d, bad, first_bad);
@@ -679,7 +688,9 @@ __device__ __forceinline__ int64_t lower_bound_adj(const int32_t *__restrict__ a
 
 // MODE 0: flags at run time; 1 / 2: HOT flags (see train_passes_kernel) on
 // an off-diagonal / diagonal pair, so the self-sample branch is compiled out
-// of the off-diagonal kernel.
+// of the off-diagonal kernel.  (Batched-dot chunks as in the latency pass
+// variant need 242 registers here: at one block per SM they measured 4.95
+// vs 6.03 G upd/s, so the pair kernel keeps the sequential dots.)
 //
 // Sample ids come in windows of kWin = 2 chunks: lane l of the group draws
 // flat samples l, l + G, ... of the window (the positive from the pool or the
@@ -707,11 +718,13 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
     const int64_t k = base + (sl.gid - sl.warp_base);
     if (!sl.enabled || k >= n) continue;
     const int64_t i = a.src_list ? (int64_t)__ldg(a.src_list + k) : k;
-    const int32_t *trow = a.targets ? a.targets + k * a.B : nullptr;
+    // HOT kernels run on materialized pools only (the fused draw stays in
+    // the MODE 0 kernel), so their code carries no binary searches
+    const int32_t *trow = (HOT || a.targets) ? a.targets + k * a.B : nullptr;
     // pool side of this source: either the materialized row or the fused draw
     int64_t first = 0, cnt = 0;
     uint64_t pkey = 0;
-    if (trow == nullptr) {
+    if (!HOT && trow == nullptr) {
       const int64_t v = a.lo_s + i;
       const int64_t e0 = __ldg(a.xadj + v), e1 = __ldg(a.xadj + v + 1);
       first = lower_bound_adj(a.adj, e0, e1, a.lo_t);
@@ -722,9 +735,13 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
     const uint64_t key = stream_key(a.seed, a.side, 1, (uint64_t)i);
     Row S;
     bool loaded = false;
-    for (int c0 = 0; c0 < total; c0 += kWin) {
-      int32_t mine[PL];
-      unsigned wpos = 0;  // bit w: window sample w is a live positive
+    // lane's samples of window c0 (ids, -1 = none) and the window's positive
+    // bits.  (An L2 prefetch of the next window's rows was measured and
+    // bought nothing: 6.21 vs 6.23 G upd/s.)
+    int32_t mine[PL];
+    unsigned wpos = 0;
+    auto draw_window = [&](int c0) {
+      wpos = 0;
 #pragma unroll
       for (int p = 0; p < PL; ++p) {
         const int w = g.gl + p * G;
@@ -733,7 +750,7 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
         bool pos = false;
         if (w < kWin && f < total) {
           const int t = f / per_t, q = f - t * per_t;
-          if (trow != nullptr) {
+          if (HOT || trow != nullptr) {
             const int32_t tgt = __ldg(trow + t);
             if (tgt >= 0) {  // absent slot: no positive, no negatives
               if (q == 0) {
@@ -755,9 +772,13 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
         if (G < 32) b = (b >> gbase) & ((1u << (G < 32 ? G : 0)) - 1u);
         wpos |= b << (p * G);
       }
+    };
+    for (int c0 = 0; c0 < total; c0 += kWin) {
+      draw_window(c0);
       int32_t win[kWin];
 #pragma unroll
       for (int w = 0; w < kWin; ++w) win[w] = __shfl_sync(g.gmask, mine[w / G], w % G, G);
+      const unsigned wpos_cur = wpos;
 #pragma unroll 1
       for (int h = 0; h < kWin / kChunk; ++h) {  // not unrolled: one copy of the chunk code
         int32_t ids[kChunk];
@@ -768,7 +789,7 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
           S.load(a.Msrc + i * (int64_t)a.dim, g.gl, a.dim);
           loaded = true;
         }
-        const unsigned pos_mask = (wpos >> (h * kChunk)) & ((1u << kChunk) - 1u);
+        const unsigned pos_mask = (wpos_cur >> (h * kChunk)) & ((1u << kChunk) - 1u);
         pos_count += __popc(pos_mask);
         run_chunk<Row, EXACT>(S, i, ids, pos_mask, a.Mtgt, a.dim, a.lr, reuse, diagonal, true, g,
                               bad, fast, atomic);
@@ -853,6 +874,7 @@ struct Variant {
   ListFn lists = nullptr;
   // HOT instantiations (default flags fixed at compile time); null if absent
   PassFn pass_hot = nullptr;
+  PassFn pass_fetch_hot = nullptr;  // KIND 2
   PassFn pass_pipe_hot = nullptr;
   PoolFn pool_hot = nullptr;       // off-diagonal pair
   PoolFn pool_hot_diag = nullptr;  // diagonal pair (Msrc == Mtgt)
@@ -862,13 +884,14 @@ template <class Row, bool EXACT, bool WITH_HOT = false>
 Variant make_variant() {
   Variant v;
   v.G = Row::G;
-  v.pass = train_passes_kernel<Row, EXACT, false, false>;
-  v.pass_pipe = train_passes_kernel<Row, EXACT, true, false>;
+  v.pass = train_passes_kernel<Row, EXACT, 0, false>;
+  v.pass_pipe = train_passes_kernel<Row, EXACT, 1, false>;
   v.pool = train_pool_kernel<Row, EXACT, 0>;
   v.lists = apply_lists_kernel<Row, EXACT>;
   if constexpr (WITH_HOT && !EXACT) {
-    v.pass_hot = train_passes_kernel<Row, false, false, true>;
-    v.pass_pipe_hot = train_passes_kernel<Row, false, true, true>;
+    v.pass_hot = train_passes_kernel<Row, false, 0, true>;
+    v.pass_fetch_hot = train_passes_kernel<Row, false, 2, true>;
+    v.pass_pipe_hot = train_passes_kernel<Row, false, 1, true>;
     v.pool_hot = train_pool_kernel<Row, false, 1>;
     v.pool_hot_diag = train_pool_kernel<Row, false, 2>;
   }
