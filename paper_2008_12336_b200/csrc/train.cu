@@ -93,14 +93,7 @@ bool use_hot(unsigned flags) {
 
 void select_hot(Variant &v, unsigned flags, bool diagonal, bool pool_materialized = true) {
   if (!use_hot(flags)) return;
-  static const bool fetch = [] {
-    const char *e = std::getenv("GB_PASS_FETCH");
-    return e && std::atoi(e) != 0;
-  }();
-  if (fetch && v.pass_fetch_hot)
-    v.pass = v.pass_fetch_hot;
-  else if (v.pass_hot)
-    v.pass = v.pass_hot;
+  if (v.pass_hot) v.pass = v.pass_hot;
   if (v.pass_pipe_hot) v.pass_pipe = v.pass_pipe_hot;
   PoolFn p = diagonal ? v.pool_hot_diag : v.pool_hot;
   if (p && pool_materialized) v.pool = p;

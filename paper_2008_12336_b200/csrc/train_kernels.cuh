@@ -555,8 +555,9 @@ __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &
 // G-way parallel, instead of redundantly on every lane for every source.
 // KIND 0: throughput variant (index chain inline per source); 1: latency
 // variant (capped launches): batched index fetch, batched-dot chunks and one
-// block per SM worth of registers; 2: throughput variant with the batched
-// index fetch (sequential dots, full occupancy).  HOT = true: the default flags (fast
+// block per SM worth of registers.  (The batched index fetch with sequential
+// dots at full occupancy measured 4.77 vs 5.15 G upd/s on C2 and was
+// dropped.)  HOT = true: the default flags (fast
 // sigmoid, vector-reduction write-back, no reuse) fixed at compile time --
 // the runtime-flag branches otherwise triple the unrolled code, and the
 // i-cache misses that cost show up as the top ncu stall (no_instructions).
@@ -874,7 +875,6 @@ struct Variant {
   ListFn lists = nullptr;
   // HOT instantiations (default flags fixed at compile time); null if absent
   PassFn pass_hot = nullptr;
-  PassFn pass_fetch_hot = nullptr;  // KIND 2
   PassFn pass_pipe_hot = nullptr;
   PoolFn pool_hot = nullptr;       // off-diagonal pair
   PoolFn pool_hot_diag = nullptr;  // diagonal pair (Msrc == Mtgt)
@@ -890,7 +890,6 @@ Variant make_variant() {
   v.lists = apply_lists_kernel<Row, EXACT>;
   if constexpr (WITH_HOT && !EXACT) {
     v.pass_hot = train_passes_kernel<Row, false, 0, true>;
-    v.pass_fetch_hot = train_passes_kernel<Row, false, 2, true>;
     v.pass_pipe_hot = train_passes_kernel<Row, false, 1, true>;
     v.pool_hot = train_pool_kernel<Row, false, 1>;
     v.pool_hot_diag = train_pool_kernel<Row, false, 2>;
