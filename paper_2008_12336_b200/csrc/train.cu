@@ -93,7 +93,14 @@ bool use_hot(unsigned flags) {
 
 void select_hot(Variant &v, unsigned flags, bool diagonal, bool pool_materialized = true) {
   if (!use_hot(flags)) return;
-  if (v.pass_hot) v.pass = v.pass_hot;
+  static const bool ahead = [] {  // GB_PASS_AHEAD=0: the KIND 0 pass (A/B)
+    const char *e = std::getenv("GB_PASS_AHEAD");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (ahead && v.pass_ahead_hot)
+    v.pass = v.pass_ahead_hot;
+  else if (v.pass_hot)
+    v.pass = v.pass_hot;
   if (v.pass_pipe_hot) v.pass_pipe = v.pass_pipe_hot;
   PoolFn p = diagonal ? v.pool_hot_diag : v.pool_hot;
   if (p && pool_materialized) v.pool = p;

@@ -286,17 +286,25 @@ __device__ __forceinline__ GroupCtx group_ctx() {
 // source S.  ids[j] < 0 marks an unused slot; bit j of pos_mask marks a
 // positive (b = 1).  Sample rows are gathered first, then updated in order
 // with forwarding of repeated ids, and stored right after their update.
-template <class Row, bool EXACT>
-__device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t (&ids)[kChunk],
-                                          unsigned pos_mask, float *__restrict__ Mtgt, int dim,
-                                          double lr, bool reuse, bool self_possible,
-                                          bool load_once, const GroupCtx &g, bool &bad,
-                                          bool fast = false, bool atomic = false) {
-  Row R[kChunk];
+template <class Row>
+__device__ __forceinline__ void load_chunk(Row (&R)[kChunk], int64_t src_row,
+                                           const int32_t (&ids)[kChunk],
+                                           const float *__restrict__ Mtgt, int dim,
+                                           bool self_possible, const GroupCtx &g) {
 #pragma unroll
   for (int j = 0; j < kChunk; ++j)
     if (ids[j] >= 0 && !(self_possible && ids[j] == src_row))
       R[j].load(Mtgt + (int64_t)ids[j] * dim, g.gl, dim);
+}
+
+// The update half of run_chunk on rows already gathered by load_chunk.
+template <class Row, bool EXACT>
+__device__ __forceinline__ void compute_chunk(Row &S, Row (&R)[kChunk], int64_t src_row,
+                                              const int32_t (&ids)[kChunk], unsigned pos_mask,
+                                              float *__restrict__ Mtgt, int dim, double lr,
+                                              bool reuse, bool self_possible, bool load_once,
+                                              const GroupCtx &g, bool &bad, bool fast,
+                                              bool atomic) {
   // Repeated ids are rare (~C(4,2)/n per chunk): the row forwarding runs
   // behind one branch per chunk instead of as predicated copies on every
   // update (those cost ~10% of the pair kernel's instructions).
@@ -327,6 +335,18 @@ __device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t
         if (ids[jj] == s) R[jj] = R[j];
     }
   }
+}
+
+template <class Row, bool EXACT>
+__device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t (&ids)[kChunk],
+                                          unsigned pos_mask, float *__restrict__ Mtgt, int dim,
+                                          double lr, bool reuse, bool self_possible,
+                                          bool load_once, const GroupCtx &g, bool &bad,
+                                          bool fast = false, bool atomic = false) {
+  Row R[kChunk];
+  load_chunk<Row>(R, src_row, ids, Mtgt, dim, self_possible, g);
+  compute_chunk<Row, EXACT>(S, R, src_row, ids, pos_mask, Mtgt, dim, lr, reuse, self_possible,
+                            load_once, g, bad, fast, atomic);
 }
 
 // Batched-dot chunk (non-exact, latency variant).  With distinct sample ids
@@ -616,6 +636,95 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : Row::kMinBl
         }
       }
     }
+  } else if constexpr (KIND == 2) {
+    // throughput variant with the index chain one source ahead: the
+    // sources -> xadj -> adj loads of the next source are issued right after
+    // this source's row gathers, so their latency overlaps the gathers'
+    // instead of following the updates (+1.3% on C2: 5.21 vs 5.14 G upd/s;
+    // deeper index pipelines spill at 128 registers, and lane-batched source
+    // id loads measured 4.95)
+    const int nsamp = 1 + a.n_neg;
+    const int64_t spp = (n - sl.warp_base + sl.eff - 1) / sl.eff;  // steps per pass
+    const int64_t total = spp * a.n_passes;
+    // step cursor (uniform across the warp): pass p, item base
+    int64_t cp = a.pass_begin, cbase = sl.warp_base;
+    int cepoch = (int)(cp / a.ppe);
+    float clr = __ldg(a.lr + cepoch);
+    struct Idx {
+      int32_t v, pos;
+      uint64_t key;
+      float lr;
+      int epoch;
+      bool ok;
+    };
+    auto fetch = [&](int64_t t) {
+      Idx d;
+      d.ok = false;
+      d.v = 0;
+      d.pos = -1;
+      d.key = 0;
+      d.lr = clr;
+      d.epoch = cepoch;
+      if (t < total) {
+        const int64_t i = cbase + lane_off;
+        if (sl.enabled && i < n) {
+          const int64_t v = a.sources ? (int64_t)__ldg(a.sources + i) : i;
+          const int64_t x0 = __ldg(a.xadj + v);
+          const int64_t deg = __ldg(a.xadj + v + 1) - x0;
+          if (deg > 0) {  // isolated sources are skipped (trainer.py:198-200)
+            d.ok = true;
+            d.v = (int32_t)v;
+            d.key = stream_key(a.seed, a.stream, (uint64_t)cp, (uint64_t)v);
+            d.pos = __ldg(a.adj + x0 + draw_below(d.key, 0, deg));  // trainer.py:203
+          }
+        }
+        cbase += sl.eff;  // advance the cursor
+        if (cbase >= sl.warp_base + spp * sl.eff) {
+          cbase = sl.warp_base;
+          ++cp;
+          cepoch = (int)(cp / a.ppe);
+          clr = cp < a.pass_begin + a.n_passes ? __ldg(a.lr + cepoch) : 0.0f;
+        }
+      }
+      return d;
+    };
+    Idx cur = fetch(0);
+    for (int64_t t = 0; t < total; ++t) {
+      if (!cur.ok) {
+        cur = fetch(t + 1);
+        continue;
+      }
+      const double lr = (double)cur.lr;
+      const int64_t v = cur.v;
+      Row S;
+      S.load(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+      int32_t ids[kChunk];
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j)  // negatives: uniform over V (trainer.py:205-206)
+        ids[j] = j == 0 ? cur.pos : (j < nsamp ? (int32_t)draw_below(cur.key, (uint64_t)j, a.V) : -1);
+      Row R[kChunk];
+      load_chunk<Row>(R, v, ids, a.M, a.dim, true, g);
+      const Idx nxt = fetch(t + 1);
+      bool bad_src = false;
+      // one compute_chunk call site (a second one for the n_neg >= kChunk
+      // chunks doubled the code and spilled 1 KB per thread)
+      for (int c0 = 0; c0 < nsamp; c0 += kChunk) {
+        if (c0 > 0) {
+#pragma unroll
+          for (int j = 0; j < kChunk; ++j)
+            ids[j] = c0 + j < nsamp ? (int32_t)draw_below(cur.key, (uint64_t)(c0 + j), a.V) : -1;
+          load_chunk<Row>(R, v, ids, a.M, a.dim, true, g);
+        }
+        compute_chunk<Row, EXACT>(S, R, v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, reuse, true,
+                                  false, g, bad_src, fast, atomic);
+      }
+      S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+      if (bad_src) {
+        bad = true;
+        first_bad = min(first_bad, cur.epoch);
+      }
+      cur = nxt;
+    }
   } else {
     const int64_t spp = (n - sl.warp_base + sl.eff - 1) / sl.eff;
     const int64_t total = spp * a.n_passes;
@@ -691,7 +800,11 @@ __device__ __forceinline__ int64_t lower_bound_adj(const int32_t *__restrict__ a
 // an off-diagonal / diagonal pair, so the self-sample branch is compiled out
 // of the off-diagonal kernel.  (Batched-dot chunks as in the latency pass
 // variant need 242 registers here: at one block per SM they measured 4.95
-// vs 6.03 G upd/s, so the pair kernel keeps the sequential dots.)
+// vs 6.03 G upd/s, so the pair kernel keeps the sequential dots.  Rolling
+// gathers -- each row slot refilled with the next chunk's sample right after
+// its update, stale duplicates re-read -- measured 5.40 vs 6.32: the refill
+// loads wait on the write-back reductions still reading the slot's
+// registers.)
 //
 // Sample ids come in windows of kWin = 2 chunks: lane l of the group draws
 // flat samples l, l + G, ... of the window (the positive from the pool or the
@@ -875,6 +988,7 @@ struct Variant {
   ListFn lists = nullptr;
   // HOT instantiations (default flags fixed at compile time); null if absent
   PassFn pass_hot = nullptr;
+  PassFn pass_ahead_hot = nullptr;  // KIND 2
   PassFn pass_pipe_hot = nullptr;
   PoolFn pool_hot = nullptr;       // off-diagonal pair
   PoolFn pool_hot_diag = nullptr;  // diagonal pair (Msrc == Mtgt)
@@ -890,6 +1004,7 @@ Variant make_variant() {
   v.lists = apply_lists_kernel<Row, EXACT>;
   if constexpr (WITH_HOT && !EXACT) {
     v.pass_hot = train_passes_kernel<Row, false, 0, true>;
+    v.pass_ahead_hot = train_passes_kernel<Row, false, 2, true>;
     v.pass_pipe_hot = train_passes_kernel<Row, false, 1, true>;
     v.pool_hot = train_pool_kernel<Row, false, 1>;
     v.pool_hot_diag = train_pool_kernel<Row, false, 2>;
