@@ -325,11 +325,12 @@ def run_tournament(args):
     from paper_2008_12336_b200 import tournament as tn
     dev = torch.device("cuda", local)
     B = 5
+    dim = args.dim or DIM
     G = gb.rmat_graph(SCALE, SAMPLES, SEED)
     V = G.num_vertices
-    cfg = gb.TrainConfig(dim=DIM, negative_samples=NNEG, seed=1, learning_rate=LR,
+    cfg = gb.TrainConfig(dim=dim, negative_samples=NNEG, seed=1, learning_rate=LR,
                          atomic_rows=(not args.store_rows))
-    M = torch.from_numpy(gb.init_embedding(V, DIM, 1)).to(dev)
+    M = torch.from_numpy(gb.init_embedding(V, dim, 1)).to(dev)
 
     vr = max(1, args.virtual_ranks)
 
@@ -363,7 +364,7 @@ def run_tournament(args):
         total_ms = float(t.item())
     value = upd / (total_ms / 1000.0)  # pos_updates are already summed over ranks
     K = 2 * world if world > 1 else 2 * vr
-    bpu = 8 * DIM + (8 * DIM) / (B * (1 + NNEG))
+    bpu = 8 * dim + (8 * dim) / (B * (1 + NNEG))
     peak, peak_src = measured_peak()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -371,7 +372,8 @@ def run_tournament(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32 rows / f64 dot",
         "data": "synthetic R-MAT generated on device (seeded, Graph500 parameters)",
         "config": workload_config({
-            "workload": f"part-pair tournament on the C2 graph, K={K} parts, B={B}, d={DIM}",
+            "workload": f"part-pair tournament on the C2 graph, K={K} parts, B={B}, d={dim}",
+            "dim": dim,
             "step": "one rotation: K(K+1)/2 pairs, K-1 part exchanges",
             "parallelism": f"tournament over {world} GPU(s)"
                            + (f" ({vr} virtual ranks)" if world == 1 and vr > 1 else ""),
@@ -397,6 +399,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", choices=["c2", "tournament"], default="c2")
+    ap.add_argument("--dim", type=int, default=0,
+                    help="tournament workload: embedding dimension (default 128; C5 uses 256)")
     ap.add_argument("--virtual-ranks", type=int, default=1,
                     help="tournament on one GPU: run the schedule of R ranks (K = 2R parts) "
                          "in this process")
