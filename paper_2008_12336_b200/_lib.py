@@ -16,7 +16,8 @@ import torch
 from .errors import MlembedError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgosh_b200.so")
+# GB_LIB_PATH: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("GB_LIB_PATH") or os.path.join(_HERE, "libgosh_b200.so")
 
 GB_OK = 0
 GB_E_INVALID = -1

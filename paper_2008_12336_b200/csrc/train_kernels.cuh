@@ -38,7 +38,12 @@ constexpr double kClamp = 10.0;  // SIGMOID_CLAMP, trainer.py:35
 // dim == 4*G*NV: lane l holds float4 number k*G + l (k < NV); fully coalesced
 // 16-byte accesses, one 128-byte line per 8 lanes.
 // kMinBlocks: resident 256-thread blocks per SM the register budget targets.
-constexpr int min_blocks_for(int elems) { return elems >= 16 ? 2 : (elems >= 8 ? 3 : 4); }
+#ifndef GB_MINB_E16
+#define GB_MINB_E16 2  // -DGB_MINB_E16=3: 80 registers, ~1 KB spills, C2 2.91 vs 5.22 G upd/s
+#endif
+constexpr int min_blocks_for(int elems) {
+  return elems >= 16 ? GB_MINB_E16 : (elems >= 8 ? 3 : 4);
+}
 
 template <int G_, int NV>
 struct VecRow {
