@@ -297,7 +297,11 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": non_iso * bps,
-                     "bytes_per_source": bps, "kernel_ms": kern_ms, "peak_source": peak_src},
+                     "bytes_per_source": bps, "kernel_ms": kern_ms, "peak_source": peak_src,
+                     # real DRAM bytes (ncu, per launch) over the live kernel time: hub rows
+                     # hit in L2, so this is below the algorithmic fraction
+                     "dram_frac": (traffic / (kern_ms / 1000.0) / 1e9 / peak
+                                   if traffic else None)},
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": V * DIM * 4, "d2h_bytes_per_step": V * DIM * 4,
                 "step": f"train_level(g, M_pinned_host, edge-scaled, e_i=1): {ppe} passes + "
