@@ -6,6 +6,9 @@ Modes (MODES env, comma list):
              num_workers=1, i.e. the reference's own AUCROC
   cap<N>     Hogwild with max_inflight=N (cap0 = auto policy)
   tour<R>    finest level by the part-pair tournament over R virtual ranks
+  large<K>   finest level by train_large (the reference's partitioned
+             trainer, bigtrain.py:343-493) with a budget giving K parts --
+             the single-device form of the algorithm the tournament shards
   a suffix "s" (cap0s, tour2s) writes sample rows back with plain stores
   (atomic_rows=False); the default is vector-reduction write-back
 
@@ -57,6 +60,29 @@ print(json.dumps({"graph": graph, "vertices": g.num_vertices, "arcs": g.num_edge
                   "eval_train_pairs": 2 * int(pos_train.shape[0]),
                   "eval_test_pairs": 2 * int(pos_test.shape[0]), "unit": unit,
                   "epochs": epochs, "dim": dim}), flush=True)
+def train_multilevel_large_finest(cfg, K):
+    """train_multilevel (trainer.py:252-288) with the finest level trained by
+    train_large under a budget that yields K parts (coarser levels in memory,
+    like train_multilevel_sharded's default shard_levels=1)."""
+    from paper_2008_12336_b200 import trainer as tr
+    plan = tr.epoch_plan(cfg.total_epochs, cfg.smoothing_ratio, h.depth).per_level
+    M = torch.from_numpy(gb.init_embedding(h.graphs[-1].num_vertices, cfg.dim,
+                                           cfg.seed)).cuda()
+    for i in range(h.depth - 1, -1, -1):
+        g_i, e_i = h.graphs[i], int(plan[i])
+        if e_i > 0:
+            if i == 0:
+                bud = gb.MemoryBudget(1)
+                row = bud.parts_resident * cfg.dim * 4 + bud.pools_resident * 2 * bud.batch_size * 4
+                bud = gb.MemoryBudget(-(-g_i.num_vertices // K) * row)
+                gb.train_large(g_i, M, cfg, e_i, bud, rng_stream=i)
+            else:
+                gb.train_level(g_i, M, cfg, e_i, rng_stream=i)
+        if i > 0:
+            M = gb.expand_embedding(M, h.mappings[i - 1])
+    return M
+
+
 for mode_s in modes:
     atomic = not mode_s.endswith("s")
     mode = mode_s if atomic else mode_s[:-1]
@@ -71,6 +97,8 @@ for mode_s in modes:
         if mode.startswith("tour"):
             M, _ = gb.train_multilevel_sharded(tg, cfg, hierarchy=h, num_ranks=int(mode[4:]),
                                                return_device=True)
+        elif mode.startswith("large"):
+            M = train_multilevel_large_finest(cfg, int(mode[5:]))
         else:
             M = gb.train_multilevel(tg, cfg, hierarchy=h, return_device=True)
         torch.cuda.synchronize()
