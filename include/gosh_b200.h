@@ -49,7 +49,7 @@ extern "C" {
  *   [0] non-finite flag (0/1)            -- fused replacement of the
  *   [1] first epoch that saw a non-finite    isfinite scan, trainer.py:236-237
  *   [2] positive updates applied (pool kernels; train_pair return value)
- *   [3] reserved                                                              */
+ *   [3] negative updates applied (pool kernels)                               */
 #define GB_STATUS_WORDS 4
 
 const char *gb_last_error(void);
@@ -221,6 +221,33 @@ int gb_train_pool_list(float *Msrc, float *Mtgt, int dim, const int32_t *list,
                        int n_neg, double lr, uint64_t seed, uint64_t side,
                        unsigned flags, int64_t max_groups, int64_t *status,
                        void *stream_handle);
+
+/* Balanced pools (an opt-in alternative to the reference's fixed-B pools,
+ * not in the reference): every source v in [lo_s, hi_s) with deg(v) > 0 gets
+ * an entry k < *count with list[k] = v - lo_s, first[k]/cnt[k] = its
+ * neighbours in [lo_t, hi_t) as a range of adj, and npos[k] =
+ * floor(BK*cnt/deg + u) positives (u uniform from key(seed, side, 2, v)):
+ * over a rotation of K parts with BK = B*K the positives follow the
+ * in-memory pass's neighbour distribution in expectation. */
+int gb_fill_pool_balanced(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
+                          int64_t hi_s, int64_t lo_t, int64_t hi_t, int64_t BK,
+                          uint64_t seed, uint64_t side, int32_t *list,
+                          int64_t *first, int32_t *cnt, int32_t *npos,
+                          int64_t *count, void *stream_handle);
+
+/* Pair side over balanced pools: entry k trains local source list[k] with
+ * B slots (slot t: a positive iff t < npos[k], then n_neg negatives from
+ * key(seed, side, 1, i)), then npos[k] - B further positives if npos[k] > B;
+ * positive t = adj[first[k] + draw_below(key(seed, pool_side, 0, lo_s + i),
+ * t, cnt[k])] - lo_t.  Otherwise as gb_train_pool_list. */
+int gb_train_pool_balanced(float *Msrc, float *Mtgt, int dim, const int32_t *list,
+                           const int64_t *first, const int32_t *cnt,
+                           const int32_t *npos, const int64_t *count,
+                           int64_t max_src, int B, int64_t lo_t, int64_t n_t,
+                           int n_neg, double lr, uint64_t seed, uint64_t side,
+                           const int32_t *adj, int64_t lo_s, uint64_t pool_side,
+                           unsigned flags, int64_t max_groups, int64_t *status,
+                           void *stream_handle);
 
 /* Page-lock a caller host buffer in place (cudaHostRegister) so part
  * switches of the partitioned trainer DMA straight from / into the caller's

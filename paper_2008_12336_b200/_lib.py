@@ -67,6 +67,11 @@ SIGNATURES = {
                                     _p, _p]),
     "gb_train_pool_list": (_int, [_p, _p, _int, _p, _p, _p, _i64, _int, _i64, _i64, _int, _dbl,
                                   _u64, _u64, C.c_uint, _i64, _p, _p]),
+    "gb_fill_pool_balanced": (_int, [_p, _p, _i64, _i64, _i64, _i64, _i64, _u64, _u64, _p,
+                                     _p, _p, _p, _p, _p]),
+    "gb_train_pool_balanced": (_int, [_p, _p, _int, _p, _p, _p, _p, _p, _i64, _int, _i64,
+                                      _i64, _int, _dbl, _u64, _u64, _p, _i64, _u64, C.c_uint,
+                                      _i64, _p, _p]),
     "gb_host_register": (_int, [_p, _sz]),
     "gb_host_unregister": (_int, [_p]),
     "gb_undirected_pairs_workspace": (_int, [_i64, _psz]),

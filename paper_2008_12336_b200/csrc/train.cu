@@ -91,7 +91,8 @@ bool use_hot(unsigned flags) {
          (flags & GB_TRAIN_ATOMIC) && !(flags & GB_TRAIN_REUSE);
 }
 
-void select_hot(Variant &v, unsigned flags, bool diagonal, bool pool_materialized = true) {
+void select_hot(Variant &v, unsigned flags, bool diagonal, bool pool_materialized = true,
+                bool pool_balanced = false) {
   if (!use_hot(flags)) return;
   static const bool ahead = [] {  // GB_PASS_AHEAD=0: the KIND 0 pass (A/B)
     const char *e = std::getenv("GB_PASS_AHEAD");
@@ -102,8 +103,9 @@ void select_hot(Variant &v, unsigned flags, bool diagonal, bool pool_materialize
   else if (v.pass_hot)
     v.pass = v.pass_hot;
   if (v.pass_pipe_hot) v.pass_pipe = v.pass_pipe_hot;
-  PoolFn p = diagonal ? v.pool_hot_diag : v.pool_hot;
-  if (p && pool_materialized) v.pool = p;
+  PoolFn p = pool_balanced ? (diagonal ? v.pool_bal_hot_diag : v.pool_bal_hot)
+                           : (diagonal ? v.pool_hot_diag : v.pool_hot);
+  if (p && (pool_materialized || pool_balanced)) v.pool = p;
 }
 
 bool aligned16(const void *p, int dim) {
@@ -213,7 +215,7 @@ GB_API int gb_train_pool_side(float *Msrc, float *Mtgt, int dim, const int32_t *
              "gb_train_pool_side: dim %d unsupported", dim);
   select_hot(var, flags, Msrc == Mtgt, targets != nullptr);
   PoolArgs a{Msrc, Mtgt, dim, targets, n_src, B, lo_t, n_t, n_neg, lr, seed, side, xadj, adj,
-             lo_s, pool_side, nullptr, nullptr, (flags & GB_TRAIN_REUSE) != 0,
+             lo_s, pool_side, nullptr, nullptr, nullptr, nullptr, nullptr, (flags & GB_TRAIN_REUSE) != 0,
              (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status};
   int grid = 1;
   if (!exact) {
@@ -241,9 +243,40 @@ GB_API int gb_train_pool_list(float *Msrc, float *Mtgt, int dim, const int32_t *
              "gb_train_pool_list: dim %d unsupported", dim);
   select_hot(var, flags, Msrc == Mtgt);
   PoolArgs a{Msrc, Mtgt, dim, targets, max_src, B, lo_t, n_t, n_neg, lr, seed, side, nullptr,
-             nullptr, 0, 0, list, count, (flags & GB_TRAIN_REUSE) != 0,
+             nullptr, 0, 0, list, count, nullptr, nullptr, nullptr, (flags & GB_TRAIN_REUSE) != 0,
              (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0,
              exact ? 1 : max_groups, status};
+  int grid = 1;
+  if (!exact) {
+    int rc = grid_for((const void *)var.pool, var.G, max_groups, max_src, &grid);
+    if (rc) return rc;
+  }
+  var.pool<<<grid, kBlock, 0, as_stream(stream_handle)>>>(a);
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
+GB_API int gb_train_pool_balanced(float *Msrc, float *Mtgt, int dim, const int32_t *list,
+                                  const int64_t *first, const int32_t *cnt, const int32_t *npos,
+                                  const int64_t *count, int64_t max_src, int B, int64_t lo_t,
+                                  int64_t n_t, int n_neg, double lr, uint64_t seed,
+                                  uint64_t side, const int32_t *adj, int64_t lo_s,
+                                  uint64_t pool_side, unsigned flags, int64_t max_groups,
+                                  int64_t *status, void *stream_handle) {
+  GB_REQUIRE(dim >= 1 && B >= 1 && n_neg >= 0 && max_src >= 0 && n_t >= 0,
+             "gb_train_pool_balanced: bad sizes");
+  GB_REQUIRE(Msrc && Mtgt && status && list && first && cnt && npos && count && adj,
+             "gb_train_pool_balanced: null pointer");
+  if (max_src == 0 || n_t == 0) return GB_OK;
+  const bool exact = flags & GB_TRAIN_EXACT;
+  Variant var;
+  GB_REQUIRE(pick_variant(dim, aligned16(Msrc, dim) && aligned16(Mtgt, dim), exact, var),
+             "gb_train_pool_balanced: dim %d unsupported", dim);
+  select_hot(var, flags, Msrc == Mtgt, false, true);
+  PoolArgs a{Msrc, Mtgt, dim, nullptr, max_src, B, lo_t, n_t, n_neg, lr, seed, side, nullptr,
+             adj, lo_s, pool_side, list, count, first, cnt, npos,
+             (flags & GB_TRAIN_REUSE) != 0, (flags & GB_TRAIN_FAST_SIGMOID) != 0,
+             !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status};
   int grid = 1;
   if (!exact) {
     int rc = grid_for((const void *)var.pool, var.G, max_groups, max_src, &grid);
@@ -344,9 +377,72 @@ __global__ void fill_pool_compact_kernel(const int64_t *__restrict__ xadj,
     }
   }
 }
+
+// Balanced pool side: every source with a neighbour anywhere gets an entry;
+// its positives in this pair number npos = floor(BK*cnt/deg + u), u uniform
+// from key(seed, side, 2, v) -- in expectation the share of BK positives
+// (B per pass-equivalent, K parts) that the in-memory pass would draw from
+// the part's cnt of its deg neighbours.  Positives are drawn in the pair
+// kernel from adj[first .. first + cnt).
+__global__ void fill_pool_balanced_kernel(const int64_t *__restrict__ xadj,
+                                          const int32_t *__restrict__ adj, int64_t lo_s,
+                                          int64_t hi_s, int64_t lo_t, int64_t hi_t, int64_t BK,
+                                          uint64_t seed, uint64_t side,
+                                          int32_t *__restrict__ list, int64_t *__restrict__ first,
+                                          int32_t *__restrict__ cnt_out,
+                                          int32_t *__restrict__ npos_out,
+                                          unsigned long long *count) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t v0 = lo_s + (int64_t)blockIdx.x * blockDim.x; v0 < hi_s;
+       v0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = v0 + threadIdx.x;
+    int64_t f = 0, cnt = 0, deg = 0;
+    if (v < hi_s) {
+      const int64_t e0 = __ldg(xadj + v), e1 = __ldg(xadj + v + 1);
+      deg = e1 - e0;
+      if (deg > 0) {
+        f = lower_bound_adj(adj, e0, e1, lo_t);
+        cnt = lower_bound_adj(adj, f, e1, hi_t) - f;
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, deg > 0);
+    if (m == 0) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(count, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (deg > 0) {
+      const int64_t slot = (int64_t)base + __popc(m & ((1u << lane) - 1u));
+      const double share = __ddiv_rn((double)(BK * cnt), (double)deg);
+      const double u = draw_unit(stream_key(seed, side, 2, (uint64_t)v), 0);
+      list[slot] = (int32_t)(v - lo_s);
+      first[slot] = f;
+      cnt_out[slot] = (int32_t)cnt;
+      npos_out[slot] = cnt > 0 ? (int32_t)floor(__dadd_rn(share, u)) : 0;
+    }
+  }
+}
 }  // namespace
 }  // namespace tk
 }  // namespace gb
+
+GB_API int gb_fill_pool_balanced(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
+                                 int64_t hi_s, int64_t lo_t, int64_t hi_t, int64_t BK,
+                                 uint64_t seed, uint64_t side, int32_t *list, int64_t *first,
+                                 int32_t *cnt, int32_t *npos, int64_t *count,
+                                 void *stream_handle) {
+  GB_REQUIRE(xadj && adj && list && first && cnt && npos && count && BK >= 1 &&
+                 hi_s >= lo_s && hi_t >= lo_t,
+             "gb_fill_pool_balanced: bad args");
+  GB_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int64_t), as_stream(stream_handle)));
+  const int64_t n = hi_s - lo_s;
+  if (n == 0) return GB_OK;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+  gb::tk::fill_pool_balanced_kernel<<<(int)blocks, 256, 0, as_stream(stream_handle)>>>(
+      xadj, adj, lo_s, hi_s, lo_t, hi_t, BK, seed, side, list, first, cnt, npos,
+      reinterpret_cast<unsigned long long *>(count));
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
 
 GB_API int gb_fill_pool_compact(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
                                 int64_t hi_s, int64_t lo_t, int64_t hi_t, int B, uint64_t seed,

@@ -782,6 +782,11 @@ struct PoolArgs {
   // first min(n_src, *n_list) entries are live.  Null: source k is k.
   const int32_t *__restrict__ src_list;
   const int64_t *__restrict__ n_list;
+  // balanced pools (gb_fill_pool_balanced): entry k draws bal_npos[k]
+  // positives from adj[bal_first[k] .. + bal_cnt[k]) on the fly; null: off
+  const int64_t *__restrict__ bal_first;
+  const int32_t *__restrict__ bal_cnt;
+  const int32_t *__restrict__ bal_npos;
   bool reuse;
   bool fast;
   bool atomic;
@@ -825,14 +830,16 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
   const Slots<Row> sl(a.max_groups);
   if (sl.warp_idle()) return;
   constexpr bool HOT = MODE != 0;
+  constexpr bool BALC = MODE >= 3;  // HOT on balanced pools
   const bool fast = HOT || a.fast, atomic = HOT || a.atomic, reuse = !HOT && a.reuse;
-  const bool diagonal = HOT ? MODE == 2 : a.Msrc == a.Mtgt;
+  const bool diagonal = HOT ? (MODE == 2 || MODE == 4) : a.Msrc == a.Mtgt;
+  const bool bal = BALC || (!HOT && a.bal_npos != nullptr);
   const int per_t = 1 + a.n_neg;
   const int total = a.B * per_t;
   const int gbase = (int)(threadIdx.x & 31) - g.gl;
   const int64_t n = a.src_list ? min(a.n_src, *a.n_list) : a.n_src;
   bool bad = false;
-  unsigned long long pos_count = 0;
+  unsigned long long pos_count = 0, neg_count = 0;
 
   for (int64_t base = sl.warp_base; base < n; base += sl.eff) {
     const int64_t k = base + (sl.gid - sl.warp_base);
@@ -840,11 +847,20 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
     const int64_t i = a.src_list ? (int64_t)__ldg(a.src_list + k) : k;
     // HOT kernels run on materialized pools only (the fused draw stays in
     // the MODE 0 kernel), so their code carries no binary searches
-    const int32_t *trow = (HOT || a.targets) ? a.targets + k * a.B : nullptr;
-    // pool side of this source: either the materialized row or the fused draw
+    const bool mat = !bal && (HOT || a.targets != nullptr);
+    const int32_t *trow = mat ? a.targets + k * a.B : nullptr;
+    // pool side of this source: the materialized row, the balanced entry
+    // or the fused draw
     int64_t first = 0, cnt = 0;
     uint64_t pkey = 0;
-    if (!HOT && trow == nullptr) {
+    int npos = 0, tot = total;
+    if (bal) {
+      first = __ldg(a.bal_first + k);
+      cnt = __ldg(a.bal_cnt + k);
+      npos = __ldg(a.bal_npos + k);
+      pkey = stream_key(a.seed, a.pool_side, 0, (uint64_t)(a.lo_s + i));
+      tot = total + max(0, npos - a.B);
+    } else if (!HOT && trow == nullptr) {
       const int64_t v = a.lo_s + i;
       const int64_t e0 = __ldg(a.xadj + v), e1 = __ldg(a.xadj + v + 1);
       first = lower_bound_adj(a.adj, e0, e1, a.lo_t);
@@ -868,9 +884,23 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
         const int f = c0 + w;
         int32_t id = -1;
         bool pos = false;
-        if (w < kWin && f < total) {
+        if (w < kWin && f < tot) {
           const int t = f / per_t, q = f - t * per_t;
-          if (HOT || trow != nullptr) {
+          if (bal) {
+            // slots t < B: positive iff t < npos, then n_neg negatives; the
+            // positives beyond B follow one per sample (gb_fill_pool_balanced)
+            if (f >= total) {
+              id = (int32_t)(__ldg(a.adj + first + draw_below(pkey, (uint64_t)(a.B + f - total), cnt)) - a.lo_t);
+              pos = true;
+            } else if (q == 0) {
+              if (t < npos) {
+                id = (int32_t)(__ldg(a.adj + first + draw_below(pkey, (uint64_t)t, cnt)) - a.lo_t);
+                pos = true;
+              }
+            } else {
+              id = (int32_t)draw_below(key, (uint64_t)(t * a.n_neg + (q - 1)), a.n_t);
+            }
+          } else if (mat) {
             const int32_t tgt = __ldg(trow + t);
             if (tgt >= 0) {  // absent slot: no positive, no negatives
               if (q == 0) {
@@ -893,7 +923,7 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
         wpos |= b << (p * G);
       }
     };
-    for (int c0 = 0; c0 < total; c0 += kWin) {
+    for (int c0 = 0; c0 < tot; c0 += kWin) {
       draw_window(c0);
       int32_t win[kWin];
 #pragma unroll
@@ -911,6 +941,8 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
         }
         const unsigned pos_mask = (wpos_cur >> (h * kChunk)) & ((1u << kChunk) - 1u);
         pos_count += __popc(pos_mask);
+        neg_count += (ids[0] >= 0) + (ids[1] >= 0) + (ids[2] >= 0) + (ids[3] >= 0) -
+                     __popc(pos_mask);
         run_chunk<Row, EXACT>(S, i, ids, pos_mask, a.Mtgt, a.dim, a.lr, reuse, diagonal, true, g,
                               bad, fast, atomic);
       }
@@ -919,6 +951,7 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
   }
   if (g.gl == 0) {
     if (pos_count) atomicAdd(reinterpret_cast<unsigned long long *>(a.status + 2), pos_count);
+    if (neg_count) atomicAdd(reinterpret_cast<unsigned long long *>(a.status + 3), neg_count);
     if (bad) {
       atomicOr(reinterpret_cast<unsigned long long *>(a.status), 1ull);
       atomicMin(reinterpret_cast<long long *>(a.status + 1), 0ll);
@@ -998,6 +1031,8 @@ struct Variant {
   PassFn pass_pipe_hot = nullptr;
   PoolFn pool_hot = nullptr;       // off-diagonal pair
   PoolFn pool_hot_diag = nullptr;  // diagonal pair (Msrc == Mtgt)
+  PoolFn pool_bal_hot = nullptr;   // balanced pools
+  PoolFn pool_bal_hot_diag = nullptr;
 };
 
 template <class Row, bool EXACT, bool WITH_HOT = false>
@@ -1014,6 +1049,8 @@ Variant make_variant() {
     v.pass_pipe_hot = train_passes_kernel<Row, false, 1, true>;
     v.pool_hot = train_pool_kernel<Row, false, 1>;
     v.pool_hot_diag = train_pool_kernel<Row, false, 2>;
+    v.pool_bal_hot = train_pool_kernel<Row, false, 3>;
+    v.pool_bal_hot_diag = train_pool_kernel<Row, false, 4>;
   }
   return v;
 }

@@ -144,7 +144,8 @@ class PairStep:
 PairFn = Callable[[torch.Tensor, torch.Tensor, PairStep], None]
 
 
-def device_pair_fn(g: Graph, cfg: TrainConfig, B: int) -> tuple[PairFn, torch.Tensor]:
+def device_pair_fn(g: Graph, cfg: TrainConfig, B: int,
+                   K: int = 1) -> tuple[PairFn, torch.Tensor]:
     """Pair step on the GPU: side 2 then side 3 (bigtrain.py:241-260) through
     bigtrain.PairSides (compacted pools + list pair kernel by default);
     returns (fn, status block)."""
@@ -155,7 +156,7 @@ def device_pair_fn(g: Graph, cfg: TrainConfig, B: int) -> tuple[PairFn, torch.Te
         _lib.GB_TRAIN_ATOMIC if cfg.atomic_rows and not cfg.deterministic else 0)
     status = _lib.new_status()
     n_s = cfg.negative_samples
-    side_step = PairSides(csr, cfg, flags, B, status)
+    side_step = PairSides(csr, cfg, flags, B, status, K=K)
 
     def fn(Ma: torch.Tensor, Mb: torch.Tensor, s: PairStep) -> None:
         if s.hi_a - s.lo_a <= 0 or s.hi_b - s.lo_b <= 0:
@@ -259,7 +260,7 @@ def train_tournament(g: Graph, M, cfg: TrainConfig, e_i: int, batch_size: int = 
     moves = shift_moves(K)
     status = None
     if pair_fn is None:
-        pair_fn, status = device_pair_fn(g, cfg, B)
+        pair_fn, status = device_pair_fn(g, cfg, B, K)
         device = torch.device("cuda", torch.cuda.current_device())
     else:
         device = M.device if isinstance(M, torch.Tensor) else torch.device("cpu")
@@ -307,18 +308,20 @@ def train_tournament(g: Graph, M, cfg: TrainConfig, e_i: int, batch_size: int = 
         torch.cuda.current_stream(device).synchronize()
     train_s = time.perf_counter() - t0
 
-    pos_local = 0
+    pos_local = neg_local = 0
     if status is not None:
         st = status.cpu().tolist()
         if st[0]:
             raise FloatingPointError("non-finite embedding after tournament training")
-        pos_local = int(st[2])
-    pos = pos_local
+        pos_local, neg_local = int(st[2]), int(st[3])
+    else:  # checker pair_fn: the reference's pools, n_neg negatives per positive
+        neg_local = pos_local * cfg.negative_samples
+    pos, neg = pos_local, neg_local
     if distributed:
-        t = torch.tensor([pos_local, n_pairs, sent_bytes], dtype=torch.int64,
+        t = torch.tensor([pos_local, neg_local, n_pairs, sent_bytes], dtype=torch.int64,
                          device=device if dist.get_backend(group) == "nccl" else "cpu")
         dist.all_reduce(t, group=group)
-        pos, n_pairs, sent_bytes = (int(x) for x in t.tolist())
+        pos, neg, n_pairs, sent_bytes = (int(x) for x in t.tolist())
 
     if gather:
         _gather(Mt, parts, plan, G, rank, distributed, group, device)
@@ -333,7 +336,7 @@ def train_tournament(g: Graph, M, cfg: TrainConfig, e_i: int, batch_size: int = 
         "rounds_per_rotation": len(rounds),
         "pairs": n_pairs,
         "pos_updates": pos,
-        "neg_updates": pos * cfg.negative_samples,
+        "neg_updates": neg,
         "exchange_bytes": sent_bytes,
         "train_s": train_s,
     }

@@ -62,6 +62,8 @@ class TrainConfig:
     deterministic: bool = False
     max_inflight: int = 0
     atomic_rows: bool = True
+    # partitioned / sharded trainers only: balanced pools (bigtrain.PairSides)
+    balanced_pools: bool = False
 
     def validate(self) -> None:
         if self.dim < 1:
@@ -80,6 +82,8 @@ class TrainConfig:
             raise ConfigError(f"epoch_unit must be one of {EPOCH_UNITS}")
         if self.max_inflight < 0:
             raise ConfigError("max_inflight must be >= 0")
+        if self.balanced_pools and self.deterministic:
+            raise ConfigError("balanced_pools runs on the Hogwild kernels (deterministic=False)")
 
 
 @dataclass

@@ -9,6 +9,7 @@ Modes (MODES env, comma list):
   large<K>   finest level by train_large (the reference's partitioned
              trainer, bigtrain.py:343-493) with a budget giving K parts --
              the single-device form of the algorithm the tournament shards
+  a suffix "b" (tour8b, large16b) uses balanced pools (TrainConfig.balanced_pools)
   a suffix "s" (cap0s, tour2s) writes sample rows back with plain stores
   (atomic_rows=False); the default is vector-reduction write-back
 
@@ -84,14 +85,16 @@ def train_multilevel_large_finest(cfg, K):
 
 
 for mode_s in modes:
-    atomic = not mode_s.endswith("s")
-    mode = mode_s if atomic else mode_s[:-1]
+    balanced = mode_s.endswith("b")  # tour<R>b / large<K>b: balanced pools
+    mode = mode_s[:-1] if balanced else mode_s
+    atomic = not mode.endswith("s")
+    mode = mode if atomic else mode[:-1]
     for seed in seeds:
         cfg = gb.TrainConfig(dim=dim, total_epochs=epochs, smoothing_ratio=0.3,
                              learning_rate=0.035, negative_samples=3, seed=seed,
                              epoch_unit=unit, deterministic=mode == "det",
                              max_inflight=int(mode[3:]) if mode.startswith("cap") else 0,
-                             atomic_rows=atomic)
+                             atomic_rows=atomic, balanced_pools=balanced)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         if mode.startswith("tour"):

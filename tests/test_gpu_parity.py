@@ -504,6 +504,114 @@ def test_tournament_pool_modes_agree(cuda, monkeypatch):
     assert _rel_err(outs["compact"][1], outs["fused"][1]) < 0.05
 
 
+def _balanced_fill_host(orc, x, a, lo_s, hi_s, lo_t, hi_t, BK, seed, side):
+    """Host restatement of gb_fill_pool_balanced (entries in source order)."""
+    out = []
+    for v in range(lo_s, hi_s):
+        e0, e1 = int(x[v]), int(x[v + 1])
+        deg = e1 - e0
+        if deg == 0:
+            continue
+        row = a[e0:e1]
+        f = e0 + int(np.searchsorted(row, lo_t, "left"))
+        cnt = e0 + int(np.searchsorted(row, hi_t, "left")) - f
+        u = orc.draw_below(orc.stream_key(seed, side, 2, v), 0, 1 << 53) * 2.0 ** -53
+        npos = int(np.floor(BK * cnt / deg + u)) if cnt else 0
+        out.append((v - lo_s, f, cnt, npos))
+    return np.array(out, dtype=np.int64).reshape(-1, 4)
+
+
+def _balanced_fill_device(G, lo_s, hi_s, lo_t, hi_t, BK, seed, side):
+    xa, aa = G.device_csr()
+    n = hi_s - lo_s
+    lst = torch.empty(n, dtype=torch.int32, device="cuda")
+    first = torch.empty(n, dtype=torch.int64, device="cuda")
+    cnt = torch.empty(n, dtype=torch.int32, device="cuda")
+    npos = torch.empty(n, dtype=torch.int32, device="cuda")
+    count = torch.empty(1, dtype=torch.int64, device="cuda")
+    _lib.call("gb_fill_pool_balanced", _lib.ptr(xa), _lib.ptr(aa), lo_s, hi_s, lo_t, hi_t, BK,
+              _lib.u64(seed), side, _lib.ptr(lst), _lib.ptr(first), _lib.ptr(cnt),
+              _lib.ptr(npos), _lib.ptr(count), _lib.stream())
+    c = int(count.item())
+    t = np.stack([lst[:c].cpu().numpy(), first[:c].cpu().numpy(), cnt[:c].cpu().numpy(),
+                  npos[:c].cpu().numpy()], axis=1).astype(np.int64)
+    return t[np.argsort(t[:, 0], kind="stable")]
+
+
+def test_balanced_pool_fill_matches_host(cuda, orc):
+    x, a = orc.rmat_graph(11, 16000, 4, densify_ids=True)
+    G = Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
+    n = G.num_vertices
+    lo_s, hi_s, lo_t, hi_t = n // 4, n // 2, n // 2, 3 * n // 4
+    got = _balanced_fill_device(G, lo_s, hi_s, lo_t, hi_t, 40, 99, 1)
+    want = _balanced_fill_host(orc, x, a, lo_s, hi_s, lo_t, hi_t, 40, 99, 1)
+    assert np.array_equal(got, want)
+    assert (want[:, 3] > 5).any() and (want[:, 3] == 0).any()
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_balanced_pair_kernel_serial(cuda, orc, exact):
+    """gb_train_pool_balanced run serially over a sorted entry list equals the
+    host replay of its sample sequence through update_embedding: bit-exact
+    with EXACT kernels, within 1e-5 for the HOT (tree-dot) kernel."""
+    x, a = orc.rmat_graph(10, 12000, 6, densify_ids=True)
+    G = Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
+    n = G.num_vertices
+    lo_s, hi_s, lo_t, hi_t = 0, n // 2, n // 2, n
+    ns, nt = hi_s - lo_s, hi_t - lo_t
+    B, K, n_neg, lr, seed, dim = 5, 4, 3, 0.0625, 21, 32
+    ent = _balanced_fill_host(orc, x, a, lo_s, hi_s, lo_t, hi_t, B * K, seed, 0)
+    M0 = orc.init_embedding(n, dim, 2) * np.float32(30.0)
+    ref = np.ascontiguousarray(np.concatenate([M0[lo_s:hi_s], M0[lo_t:hi_t]]))
+    pos = 0
+    for i, f, cnt, npos in ent.tolist():
+        pkey = orc.stream_key(seed, 0, 0, lo_s + i)
+        key = orc.stream_key(seed, 2, 1, i)
+        for t in range(max(B, npos)):
+            if t < npos:
+                s_ = int(a[f + orc.draw_below(pkey, t, cnt)]) - lo_t
+                orc.update_embedding(ref, i, ns + s_, 1, lr)
+                pos += 1
+            if t < B:
+                for q in range(n_neg):
+                    orc.update_embedding(ref, i, ns + orc.draw_below(key, t * n_neg + q, nt), 0,
+                                         lr)
+    dj = torch.from_numpy(M0[lo_s:hi_s].copy()).cuda()
+    dk = torch.from_numpy(M0[lo_t:hi_t].copy()).cuda()
+    dev = [torch.from_numpy(np.ascontiguousarray(ent[:, c].astype(dt))).cuda()
+           for c, dt in ((0, np.int32), (1, np.int64), (2, np.int32), (3, np.int32))]
+    dc = torch.tensor([len(ent)], dtype=torch.int64, device="cuda")
+    st = _lib.new_status()
+    flags = _lib.GB_TRAIN_EXACT if exact else _lib.GB_TRAIN_FAST_SIGMOID | _lib.GB_TRAIN_ATOMIC
+    _lib.call("gb_train_pool_balanced", _lib.ptr(dj), _lib.ptr(dk), dim, *[_lib.ptr(t) for t in dev],
+              _lib.ptr(dc), ns, B, lo_t, nt, n_neg, lr, seed, 2, _lib.ptr(G.device_csr()[1]),
+              lo_s, 0, flags, 1, _lib.ptr(st), _lib.stream())
+    got = np.concatenate([dj.cpu().numpy(), dk.cpu().numpy()])
+    assert int(st[2]) == pos and int(st[3]) == len(ent) * B * n_neg
+    if exact:
+        assert np.array_equal(got, ref)
+    else:
+        assert _rel_err(got, ref) <= REL_TOL
+
+
+def test_tournament_balanced_pools_counts(cuda):
+    """Balanced pools in the tournament: B*n_neg negatives per source per pair
+    side, and B*K positives per source per rotation in expectation."""
+    from paper_2008_12336_b200 import tournament as tn
+    G = gb.rmat_graph(12, 40000, 5, densify_ids=True)
+    cfg = gb.TrainConfig(dim=32, seed=3, negative_samples=3, balanced_pools=True)
+    M = torch.from_numpy(gb.init_embedding(G.num_vertices, 32, 3)).cuda()
+    st = tn.train_tournament(G, M, cfg, 1, batch_size=5, num_ranks=2)
+    K, R = st["K"], st["rotations"]
+    non_iso = int((np.diff(G.xadj) > 0).sum())
+    assert st["neg_updates"] == R * non_iso * K * 5 * 3
+    want = R * non_iso * K * 5
+    assert abs(st["pos_updates"] - want) < 0.01 * want
+    assert torch.isfinite(M).all()
+    with pytest.raises(gb.ConfigError):
+        gb.TrainConfig(balanced_pools=True, deterministic=True).validate()
+
+
 def test_train_large_deterministic_bit_exact(cuda, golden):
     g = golden("large.npz")
     G = _graphs(g)[0]
