@@ -35,8 +35,7 @@ on the GPU.
 """
 from __future__ import annotations
 
-import os
-
+import dataclasses
 import time
 from dataclasses import dataclass
 from typing import Callable
@@ -378,17 +377,25 @@ def sequential_order(K: int, rotations: int):
 def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
                              shard_levels: int = 1, batch_size: int = 5, group=None,
                              num_ranks: int | None = None, hierarchy=None,
-                             return_device: bool = False):
+                             return_device: bool = False, balanced_pools: bool = True):
     """train_multilevel (trainer.py:252-288) with the finest `shard_levels`
     levels trained by the tournament across ranks.  Every rank coarsens
     (the device collapse is deterministic, so the hierarchies are identical
     with no communication); the coarse levels train on rank 0 and the matrix
     is broadcast before the first sharded level.  Returns
-    (matrix, per-level stats)."""
+    (matrix, per-level stats).
+
+    balanced_pools (default; Hogwild runs only): the sharded levels draw
+    balanced pools (TrainConfig.balanced_pools), which keeps this path's
+    AUCROC at the in-memory pass's (C3: 0.823-0.829 vs 0.826) where the
+    reference's fixed-B pools of train_large lose 0.04 (DESIGN.md 6);
+    False keeps the reference's pools."""
     from .coarsen import coarsen_all
     from .trainer import epoch_plan, expand_embedding, init_embedding, train_level
     import torch.distributed as dist
     cfg.validate()
+    if balanced_pools and not cfg.deterministic and not cfg.balanced_pools:
+        cfg = dataclasses.replace(cfg, balanced_pools=True)
     distributed = dist.is_available() and dist.is_initialized()
     rank = dist.get_rank(group) if distributed else 0
     if hierarchy is None:
