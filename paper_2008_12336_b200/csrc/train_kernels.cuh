@@ -815,7 +815,7 @@ __device__ __forceinline__ int64_t lower_bound_adj(const int32_t *__restrict__ a
 // gathers -- each row slot refilled with the next chunk's sample right after
 // its update, stale duplicates re-read -- measured 5.40 vs 6.32: the refill
 // loads wait on the write-back reductions still reading the slot's
-// registers.)
+// registers; with the refill delayed by one sample, 5.14 vs 6.26.)
 //
 // Sample ids come in windows of kWin = 2 chunks: lane l of the group draws
 // flat samples l, l + G, ... of the window (the positive from the pool or the
@@ -923,85 +923,6 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
         wpos |= b << (p * G);
       }
     };
-#ifdef GB_POOL_ROLL
-    // Experimental: rolling gathers with a one-sample delay -- the slot of
-    // sample m-1 is refilled with sample m+3 after sample m trains, so its
-    // write-back reduction has had an update's time to read its registers.
-    auto draw4 = [&](int c0, int32_t(&ids)[kChunk], unsigned &pm) {
-      draw_window(c0);  // lanes draw 8; the first 4 are this chunk
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) ids[j] = __shfl_sync(g.gmask, mine[j / G], j % G, G);
-      pm = wpos & ((1u << kChunk) - 1u);
-    };
-    int32_t ic[kChunk], in[kChunk];
-    unsigned pc = 0, pn = 0;
-    draw4(0, ic, pc);
-    if (ic[0] < 0 && ic[1] < 0 && ic[2] < 0 && ic[3] < 0) continue;
-    S.load(a.Msrc + i * (int64_t)a.dim, g.gl, a.dim);
-    loaded = true;
-    Row R[kChunk];
-    auto live = [&](int32_t x) { return x >= 0 && !(diagonal && x == i); };
-    unsigned stale = 0;
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      bool st = false;
-#pragma unroll
-      for (int jj = 0; jj < j; ++jj) st |= ic[jj] == ic[j];
-      if (live(ic[j])) {
-        if (st) stale |= 1u << j;
-        else R[j].load(a.Mtgt + (int64_t)ic[j] * a.dim, g.gl, a.dim);
-      }
-    }
-    for (int c0 = 0; c0 < tot; c0 += kChunk) {
-      if (c0 + kChunk < tot) {
-        draw4(c0 + kChunk, in, pn);
-      } else {
-#pragma unroll
-        for (int j = 0; j < kChunk; ++j) in[j] = -1;
-        pn = 0;
-      }
-      pos_count += __popc(pc);
-      neg_count += (ic[0] >= 0) + (ic[1] >= 0) + (ic[2] >= 0) + (ic[3] >= 0) - __popc(pc);
-      unsigned stale_n = 0;
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) {
-        const int32_t sj = ic[j];
-        if (sj >= 0) {
-          const double b = (pc >> j) & 1u ? 1.0 : 0.0;
-          if (diagonal && sj == i) {
-            double acc = row_dot<Row, EXACT>(S, S, g.gmask, g.gl, a.dim);
-            float sc = nce_score(acc, b, a.lr, bad, fast && !EXACT);
-            update_self(S, sc, reuse, true);
-          } else {
-            if ((stale >> j) & 1u) R[j].load(a.Mtgt + (int64_t)sj * a.dim, g.gl, a.dim);
-            double acc = row_dot<Row, EXACT>(S, R[j], g.gmask, g.gl, a.dim);
-            float sc = nce_score(acc, b, a.lr, bad, fast && !EXACT);
-            update_pair_writeback(S, R[j], sc, reuse, atomic && !EXACT,
-                                  a.Mtgt + (int64_t)sj * a.dim, g.gl, a.dim);
-          }
-        }
-        // delayed refill of the slot that trained one sample ago
-        if (j == 0) {
-          if (live(ic[3])) {
-            if (ic[3] == ic[1] || ic[3] == ic[2]) stale |= 8u;
-            else R[3].load(a.Mtgt + (int64_t)ic[3] * a.dim, g.gl, a.dim);
-          }
-        } else {
-          const int32_t x = in[j - 1];
-          const int32_t p1 = j == 1 ? ic[2] : (j == 2 ? ic[3] : in[0]);
-          const int32_t p2 = j == 1 ? ic[3] : (j == 2 ? in[0] : in[1]);
-          if (live(x)) {
-            if (x == p1 || x == p2) stale_n |= 1u << (j - 1);
-            else R[j - 1].load(a.Mtgt + (int64_t)x * a.dim, g.gl, a.dim);
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < kChunk; ++j) ic[j] = in[j];
-      pc = pn;
-      stale = stale_n;
-    }
-#else
     for (int c0 = 0; c0 < tot; c0 += kWin) {
       draw_window(c0);
       int32_t win[kWin];
@@ -1026,7 +947,6 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
                               bad, fast, atomic);
       }
     }
-#endif
     if (loaded) S.store(a.Msrc + i * (int64_t)a.dim, g.gl, a.dim);
   }
   if (g.gl == 0) {
