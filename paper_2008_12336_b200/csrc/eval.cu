@@ -39,7 +39,7 @@ constexpr int kMaxK = 16;  // d <= 512
 // rows gathered together per warp: 8 (a 256-row mini-batch = 2 gather
 // rounds per warp) as long as the batch fits the register file
 template <int K>
-constexpr int rows_per_batch() { return K <= 4 ? 8 : (K <= 8 ? 4 : 1); }
+constexpr int rows_per_batch() { return K <= 4 ? 16 : (K <= 8 ? 4 : 1); }
 
 __device__ __forceinline__ double sigmoid_clamped(double z) {  // trainer.py:96-99
   z = fmin(fmax(z, -10.0), 10.0);
@@ -89,6 +89,29 @@ __global__ void __launch_bounds__(kFitThreads, 1)
     wl[k] = t < d ? w_s[t] : 0.0;
   }
   double b = *b_s;
+  constexpr int kRowsPerBatch = rows_per_batch<K>();
+  // One gather round covers the whole mini-batch (bs <= 16 warps x rows per
+  // batch: the reference's 256 at d <= 128): the next step's rows do not
+  // depend on w, so they are gathered while this step's gradient is reduced.
+  const bool one_round = bs <= kFitWarps * kRowsPerBatch;
+  float x[kRowsPerBatch][K];
+  int8_t yv[kRowsPerBatch];
+  auto gather = [&](int64_t i0, int m, int r0) {
+#pragma unroll
+    for (int j = 0; j < kRowsPerBatch; ++j) {
+      const int r = r0 + j * kFitWarps;
+      const bool ok = r < m;
+      const int64_t row = ok ? perm[i0 + r] : 0;
+      const float *xr = X + row * d;
+      yv[j] = ok ? y[row] : 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int t = lane + 32 * k;
+        x[j][k] = (ok && t < d) ? __ldg(xr + t) : 0.0f;
+      }
+    }
+  };
+  if (one_round && n > 0) gather(0, (int)((int64_t)bs < n ? bs : n), warp);
   for (int64_t i0 = 0; i0 < n; i0 += bs) {
     const int m = (int)((int64_t)bs < n - i0 ? (int64_t)bs : n - i0);
     double g[K];
@@ -98,23 +121,8 @@ __global__ void __launch_bounds__(kFitThreads, 1)
     // rows of this warp in batches of kRowsPerBatch: every gather of a batch
     // is issued before the first dot (the rows are random, so each gather
     // is a full memory round trip; issuing them together pays it once)
-    constexpr int kRowsPerBatch = rows_per_batch<K>();
     for (int r0 = warp; r0 < m; r0 += kFitWarps * kRowsPerBatch) {
-      float x[kRowsPerBatch][K];
-      int8_t yv[kRowsPerBatch];
-#pragma unroll
-      for (int j = 0; j < kRowsPerBatch; ++j) {
-        const int r = r0 + j * kFitWarps;
-        const bool ok = r < m;
-        const int64_t row = ok ? perm[i0 + r] : 0;
-        const float *xr = X + row * d;
-        yv[j] = ok ? y[row] : 0;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const int t = lane + 32 * k;
-          x[j][k] = (ok && t < d) ? __ldg(xr + t) : 0.0f;
-        }
-      }
+      if (!one_round) gather(i0, m, r0);
 #pragma unroll
       for (int j = 0; j < kRowsPerBatch; ++j) {
         if (r0 + j * kFitWarps >= m) break;
@@ -127,6 +135,10 @@ __global__ void __launch_bounds__(kFitThreads, 1)
         for (int k = 0; k < K; ++k) g[k] = fma((double)x[j][k], resid, g[k]);
         rs += resid;
       }
+    }
+    if (one_round && i0 + bs < n) {
+      const int64_t i1 = i0 + bs;
+      gather(i1, (int)((int64_t)bs < n - i1 ? (int64_t)bs : n - i1), warp);
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
