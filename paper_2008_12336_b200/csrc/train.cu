@@ -94,9 +94,12 @@ bool use_hot(unsigned flags) {
 void select_hot(Variant &v, unsigned flags, bool diagonal, bool pool_materialized = true,
                 bool pool_balanced = false) {
   if (!use_hot(flags)) return;
-  static const bool ahead = [] {  // GB_PASS_AHEAD=0: the KIND 0 pass (A/B)
+  // GB_PASS_AHEAD=1: the KIND 2 throughput pass (index chain one source
+  // ahead): +1.3% on C2 but -8% / -10% on C3's second and third levels
+  // (high-degree, partly L2-resident), so the inline chain is the default
+  static const bool ahead = [] {
     const char *e = std::getenv("GB_PASS_AHEAD");
-    return !(e && std::atoi(e) == 0);
+    return e && std::atoi(e) != 0;
   }();
   if (ahead && v.pass_ahead_hot)
     v.pass = v.pass_ahead_hot;
@@ -189,17 +192,6 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
       const int64_t warps = std::max<int64_t>(1, (groups + gpw - 1) / gpw);
       grid = (int)std::min<int64_t>(warps, (int64_t)num_sms() * std::max(occ1, 1));
       block = 32;
-    } else if (grid < num_sms()) {
-      // capped launch too wide for the latency variant but short of one block
-      // per SM (e.g. C3's third level: 3,941 groups = 124 blocks of 256):
-      // smaller blocks spread the groups over every SM.  GB_SPREAD=0: off.
-      const char *env = std::getenv("GB_SPREAD");
-      if (!(env && std::atoi(env) == 0)) {
-        const int64_t threads = groups * var.G;
-        const int64_t per_sm = threads / num_sms();
-        block = (int)std::max<int64_t>(32, std::min<int64_t>(kBlock, per_sm / 32 * 32));
-        grid = (int)((threads + block - 1) / block);
-      }
     }
   } else {
     block = 32;

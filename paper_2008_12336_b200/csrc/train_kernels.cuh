@@ -646,9 +646,10 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : Row::kMinBl
     // throughput variant with the index chain one source ahead: the
     // sources -> xadj -> adj loads of the next source are issued right after
     // this source's row gathers, so their latency overlaps the gathers'
-    // instead of following the updates (+1.3% on C2: 5.21 vs 5.14 G upd/s;
-    // deeper index pipelines spill at 128 registers, and lane-batched source
-    // id loads measured 4.95)
+    // instead of following the updates (+1.3% on C2: 5.21 vs 5.14 G upd/s,
+    // but 5.17 vs 5.64 and 3.84 vs 4.28 on C3's levels 1 and 2, so opt-in:
+    // GB_PASS_AHEAD=1; deeper index pipelines spill at 128 registers, and
+    // lane-batched source id loads measured 4.95)
     const int nsamp = 1 + a.n_neg;
     const int64_t spp = (n - sl.warp_base + sl.eff - 1) / sl.eff;  // steps per pass
     const int64_t total = spp * a.n_passes;
