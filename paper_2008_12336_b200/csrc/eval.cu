@@ -21,12 +21,14 @@
 // Arithmetic: features are the reference's fp32 products; dots and
 // gradients are fp64 as in numpy (summation order differs from BLAS, so fits
 // agree to rounding, not bit for bit; AUC is exact for equal scores).
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <thrust/iterator/transform_iterator.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -173,6 +175,127 @@ __global__ void __launch_bounds__(kFitThreads, 1)
   if (threadIdx.x == 0) *b_g = *b_s;
 }
 
+// The same epoch on a cluster of kClusterCtas CTAs: CTA c takes rows
+// [c*rpc, (c+1)*rpc) of every mini-batch (rpc = ceil(bs / CTAs), kRpw rows
+// per warp), reduces its warps' gradients through shared memory, publishes
+// the CTA partial in a double-buffered shared slot, and after one cluster
+// barrier every CTA sums the partials of all CTAs through DSMEM in CTA
+// order -- so every CTA applies the identical update to its own copy of w.
+// The next step's rows are gathered before the reduction (they do not
+// depend on w).  Summation order differs from the single-CTA kernel (rows
+// are split differently), so weights agree to rounding.
+constexpr int kClusterCtas = 8;
+template <int K, int kRpw>
+__global__ void __launch_bounds__(kFitThreads, 1)
+    logreg_epoch_cluster_kernel(const float *__restrict__ X, int d,
+                                const int8_t *__restrict__ y, const int64_t *__restrict__ perm,
+                                int64_t n, int bs, double step, double *__restrict__ w_g,
+                                double *__restrict__ b_g) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank();
+  extern __shared__ double sh[];
+  double *w_s = sh;                                  // [d]
+  double *part = w_s + d;                            // [kFitWarps][d]
+  double *rsum = part + (size_t)kFitWarps * d;       // [kFitWarps]
+  double *pub = rsum + kFitWarps;                    // [2][d + 1] CTA partials
+  double *b_s = pub + 2 * ((size_t)d + 1);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < d; t += blockDim.x) w_s[t] = w_g[t];
+  if (threadIdx.x == 0) *b_s = *b_g;
+  __syncthreads();
+  double wl[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int t = lane + 32 * k;
+    wl[k] = t < d ? w_s[t] : 0.0;
+  }
+  double b = *b_s;
+  const int rpc = (bs + kClusterCtas - 1) / kClusterCtas;
+  float x[kRpw][K];
+  int8_t yv[kRpw];
+  auto gather = [&](int64_t i0, int m) {
+    const int lo = crank * rpc, hi = min(m, lo + rpc);
+#pragma unroll
+    for (int j = 0; j < kRpw; ++j) {
+      const int r = lo + warp + j * kFitWarps;
+      const bool ok = r < hi;
+      const int64_t row = ok ? perm[i0 + r] : 0;
+      const float *xr = X + row * d;
+      yv[j] = ok ? y[row] : 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int t = lane + 32 * k;
+        x[j][k] = (ok && t < d) ? __ldg(xr + t) : 0.0f;
+      }
+    }
+  };
+  auto rows_of = [&](int64_t i0) { return (int)((int64_t)bs < n - i0 ? (int64_t)bs : n - i0); };
+  gather(0, rows_of(0));
+  int parity = 0;
+  for (int64_t i0 = 0; i0 < n; i0 += bs, parity ^= 1) {
+    const int m = rows_of(i0);
+    const int hi = min(m, crank * rpc + rpc);
+    double g[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) g[k] = 0.0;
+    double rs = 0.0;
+#pragma unroll
+    for (int j = 0; j < kRpw; ++j) {
+      if (crank * rpc + warp + j * kFitWarps >= hi) break;
+      double z = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) z = fma((double)x[j][k], wl[k], z);
+      z = warp_sum(z) + b;
+      const double resid = sigmoid_clamped(z) - (double)yv[j];
+#pragma unroll
+      for (int k = 0; k < K; ++k) g[k] = fma((double)x[j][k], resid, g[k]);
+      rs += resid;
+    }
+    if (i0 + bs < n) gather(i0 + bs, rows_of(i0 + bs));
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int t = lane + 32 * k;
+      if (t < d) part[(size_t)warp * d + t] = g[k];
+    }
+    if (lane == 0) rsum[warp] = rs;
+    __syncthreads();
+    double *mine = pub + (size_t)parity * (d + 1);
+    for (int t = threadIdx.x; t <= d; t += blockDim.x) {
+      double G = 0.0;
+      if (t < d) {
+        for (int q = 0; q < kFitWarps; ++q) G += part[(size_t)q * d + t];
+      } else {
+        for (int q = 0; q < kFitWarps; ++q) G += rsum[q];
+      }
+      mine[t] = G;
+    }
+    cluster.sync();  // every CTA's partial is published (and part/rsum are free)
+    for (int t = threadIdx.x; t <= d; t += blockDim.x) {
+      double G = 0.0;
+      for (int c = 0; c < kClusterCtas; ++c) G += cluster.map_shared_rank(mine, c)[t];
+      if (t < d)
+        w_s[t] = w_s[t] - (step * G) / (double)m;
+      else
+        *b_s = *b_s - step * (G / (double)m);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int t = lane + 32 * k;
+      wl[k] = t < d ? w_s[t] : 0.0;
+    }
+    b = *b_s;
+    // w_s is rewritten only after the next cluster.sync, which every thread
+    // of this CTA reaches after the reads above
+  }
+  cluster.sync();  // no CTA exits while another may still read its partials
+  if (crank == 0) {
+    for (int t = threadIdx.x; t < d; t += blockDim.x) w_g[t] = w_s[t];
+    if (threadIdx.x == 0) *b_g = *b_s;
+  }
+}
+
 __global__ void predict_kernel(const float *__restrict__ X, int d, int64_t n,
                                const double *__restrict__ w, double b,
                                double *__restrict__ out) {
@@ -284,6 +407,31 @@ int auc_plan(int64_t n, void *ws, size_t *bytes, const double *scores, const int
 template <int K>
 int launch_fit(const float *X, int d, const int8_t *y, const int64_t *perm, int64_t n, int bs,
                double step, double *w, double *b, cudaStream_t st) {
+  // cluster form for the usual batch sizes (rows per warp per CTA <= 2);
+  // GB_LOGREG_CLUSTER=0 keeps the single-CTA kernel
+  const char *env = std::getenv("GB_LOGREG_CLUSTER");
+  const bool use_cluster = !(env && std::atoi(env) == 0) &&
+                           (bs + kClusterCtas - 1) / kClusterCtas <= 2 * kFitWarps;
+  if (use_cluster) {
+    const size_t smem = sizeof(double) * ((size_t)d + (size_t)kFitWarps * d + kFitWarps +
+                                          2 * ((size_t)d + 1) + 1);
+    auto fn = logreg_epoch_cluster_kernel<K, 2>;
+    GB_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kClusterCtas, 1, 1);
+    cfg.blockDim = dim3(kFitThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kClusterCtas;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    GB_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, X, d, y, perm, n, bs, step, w, b));
+    return GB_OK;
+  }
   const size_t smem = sizeof(double) * ((size_t)d + (size_t)kFitWarps * d + kFitWarps + 1);
   GB_CUDA_TRY(cudaFuncSetAttribute(logreg_epoch_kernel<K>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
