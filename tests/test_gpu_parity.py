@@ -291,7 +291,7 @@ def test_atomic_rows_keep_concurrent_updates_of_a_hot_row(cuda, orc):
 
 
 @pytest.mark.parametrize("pipe", ["0", "1"])
-@pytest.mark.parametrize("d", [32, 128])
+@pytest.mark.parametrize("d", [16, 32, 64, 128, 256])
 def test_single_group_passes_match_sequential(cuda, orc, d, pipe, monkeypatch):
     """The parallel pass kernels (throughput and latency variants) with one
     source in flight are the reference's sequential pass up to the tree dot
