@@ -1,0 +1,9 @@
+# Final HEAD check of the session: full GPU tests, smoke, C2 bench line and
+# reference arm, tournament line, C1 run_link_prediction AUCROC (device evaluator).
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -q -m gpu 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 400 python bench.py --steps 30 --warmup 5 > gpurun_out/bench_c2.json 2>/dev/null; cut -c1-160 gpurun_out/bench_c2.json
+timeout 400 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2>/dev/null; cut -c1-160 gpurun_out/bench_ref.json
+timeout 300 python bench.py --workload tournament --steps 10 --warmup 3 > gpurun_out/tourn_k2.json 2>/dev/null; cut -c1-160 gpurun_out/tourn_k2.json
+CAPS=0 SEEDS=1,2,3,4,5 timeout 900 python scripts/c1_gpu_auc.py > gpurun_out/c1auc.jsonl 2>/dev/null; cut -c1-250 gpurun_out/c1auc.jsonl
