@@ -111,6 +111,13 @@ void select_hot(Variant &v, unsigned flags, bool diagonal, bool pool_materialize
   if (p && (pool_materialized || pool_balanced)) v.pool = p;
 }
 
+// Launch of a pair-side kernel.
+int launch_pool(const Variant &var, const PoolArgs &a, int grid, cudaStream_t st) {
+  var.pool<<<grid, kBlock, 0, st>>>(a);
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
 bool aligned16(const void *p, int dim) {
   return (reinterpret_cast<uintptr_t>(p) & 15u) == 0 && dim % 4 == 0;
 }
@@ -155,11 +162,42 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
              passes_per_epoch, lr_per_epoch, (flags & GB_TRAIN_REUSE) != 0,
              (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status};
   int grid = 1, block = kBlock;
+  size_t smem = 0;
   PassFn fn = var.pass;
   if (!exact) {
     const int64_t items = sources ? n_sources : num_vertices;
     int rc = grid_for((const void *)var.pass, var.G, max_groups, items, &grid);
     if (rc) return rc;
+    // Uncapped launches (the cap reaches the throughput variant's full
+    // occupancy) run KIND 3: sample rows staged in shared memory by cp.async,
+    // 80 registers, 3 blocks per SM -- C2 5.34 vs 5.13 G upd/s, C3's
+    // uncapped levels unchanged; capped mid-size levels lose (3.35 vs 4.28 at
+    // C3 L2: per-source latency, not occupancy, bounds them), so they keep
+    // KIND 0.  GB_PASS_SMEM=0 disables, =1 forces.
+    {
+      int occ0 = 0;
+      GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, (const void *)var.pass,
+                                                                kBlock, 0));
+      const int64_t full0 = (int64_t)num_sms() * std::max(occ0, 1) * (kBlock / var.G);
+      const int64_t want = std::min<int64_t>(max_groups > 0 ? max_groups : INT64_MAX, items);
+      const char *env = std::getenv("GB_PASS_SMEM");
+      const bool on = env ? std::atoi(env) != 0 : want >= full0;
+      if (on && var.pass_staged_hot && use_hot(flags)) var.pass = var.pass_staged_hot;
+      fn = var.pass;
+    }
+    if (var.pass_staged_hot && var.pass == var.pass_staged_hot) {
+      smem = (size_t)(kBlock / var.G) * kChunk * dim * sizeof(float);
+      GB_CUDA_TRY(cudaFuncSetAttribute((const void *)var.pass,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int occ_s = 0;
+      GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, (const void *)var.pass,
+                                                                kBlock, smem));
+      const int64_t gpb = kBlock / var.G;
+      int64_t cap = max_groups > 0 ? max_groups : INT64_MAX;
+      cap = std::min(cap, std::max<int64_t>(items, 1));
+      grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * std::max(occ_s, 1),
+                                                         (cap + gpb - 1) / gpb));
+    }
     // A launch whose in-flight cap is below what the throughput variant holds
     // on the GPU is latency-bound (small levels): switch to the latency
     // variant -- widest lane layout, batched index fetch and batched dots,
@@ -192,11 +230,12 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
       const int64_t warps = std::max<int64_t>(1, (groups + gpw - 1) / gpw);
       grid = (int)std::min<int64_t>(warps, (int64_t)num_sms() * std::max(occ1, 1));
       block = 32;
+      smem = 0;
     }
   } else {
     block = 32;
   }
-  fn<<<grid, block, 0, as_stream(stream_handle)>>>(a);
+  fn<<<grid, block, smem, as_stream(stream_handle)>>>(a);
   GB_CHECK_LAUNCH();
   return GB_OK;
 }
@@ -225,9 +264,7 @@ GB_API int gb_train_pool_side(float *Msrc, float *Mtgt, int dim, const int32_t *
     int rc = grid_for((const void *)var.pool, var.G, max_groups, n_src, &grid);
     if (rc) return rc;
   }
-  var.pool<<<grid, kBlock, 0, as_stream(stream_handle)>>>(a);
-  GB_CHECK_LAUNCH();
-  return GB_OK;
+  return launch_pool(var, a, grid, as_stream(stream_handle));
 }
 
 GB_API int gb_train_pool_list(float *Msrc, float *Mtgt, int dim, const int32_t *list,
@@ -254,9 +291,7 @@ GB_API int gb_train_pool_list(float *Msrc, float *Mtgt, int dim, const int32_t *
     int rc = grid_for((const void *)var.pool, var.G, max_groups, max_src, &grid);
     if (rc) return rc;
   }
-  var.pool<<<grid, kBlock, 0, as_stream(stream_handle)>>>(a);
-  GB_CHECK_LAUNCH();
-  return GB_OK;
+  return launch_pool(var, a, grid, as_stream(stream_handle));
 }
 
 GB_API int gb_train_pool_balanced(float *Msrc, float *Mtgt, int dim, const int32_t *list,
@@ -285,9 +320,7 @@ GB_API int gb_train_pool_balanced(float *Msrc, float *Mtgt, int dim, const int32
     int rc = grid_for((const void *)var.pool, var.G, max_groups, max_src, &grid);
     if (rc) return rc;
   }
-  var.pool<<<grid, kBlock, 0, as_stream(stream_handle)>>>(a);
-  GB_CHECK_LAUNCH();
-  return GB_OK;
+  return launch_pool(var, a, grid, as_stream(stream_handle));
 }
 
 GB_API int gb_nonfinite_scan(const float *M, int64_t count, int64_t epoch, int64_t *status,

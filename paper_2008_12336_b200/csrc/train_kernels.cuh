@@ -70,6 +70,35 @@ struct VecRow {
       __stcg(reinterpret_cast<float4 *>(row) + k * G + gl, v);
     }
   }
+  // shared-memory staging (KIND 3): lane gl's 16-byte pieces of a row go to
+  // the same positions of a dim-float shared slot by cp.async (no registers
+  // held while in flight) and come back to registers when the row trains
+  static constexpr bool kStageable = true;
+  __device__ __forceinline__ static void stage(float *slot, const float *row, int gl) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(slot + 4 * (k * G + gl));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                   "l"(row + 4 * (k * G + gl))
+                   : "memory");
+    }
+  }
+  __device__ __forceinline__ void lds(const float *slot, int gl) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const float4 v = reinterpret_cast<const float4 *>(slot)[k * G + gl];
+      x[4 * k + 0] = v.x;
+      x[4 * k + 1] = v.y;
+      x[4 * k + 2] = v.z;
+      x[4 * k + 3] = v.w;
+    }
+  }
+  __device__ __forceinline__ void sts(float *slot, int gl) const {
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+      reinterpret_cast<float4 *>(slot)[k * G + gl] =
+          make_float4(x[4 * k + 0], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
+  }
   // Hogwild write-back of increments: elements 4k0/4..+3 (one float4) by a
   // 16-byte vector reduction (red.global.add.v4.f32, performed at L2), so
   // concurrent updates of the same row are all applied instead of the last
@@ -355,6 +384,50 @@ __device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t
                             load_once, g, bad, fast, atomic);
 }
 
+// run_chunk with the sample rows staged in the group's shared slots (KIND 3,
+// vector layouts only): only the row being trained occupies registers.
+template <class Row>
+__device__ __forceinline__ void run_chunk_staged(Row &S, int64_t src_row,
+                                                 const int32_t (&ids)[kChunk], unsigned pos_mask,
+                                                 float *__restrict__ Mtgt, int dim, double lr,
+                                                 float *slots, const GroupCtx &g, bool &bad,
+                                                 bool fast, bool atomic, bool self_possible = true,
+                                                 bool load_once = false) {
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j)
+    if (ids[j] >= 0 && !(self_possible && ids[j] == src_row))
+      Row::stage(slots + j * dim, Mtgt + (int64_t)ids[j] * dim, g.gl);
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  bool dup = false;
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j)
+#pragma unroll
+    for (int jj = j + 1; jj < kChunk; ++jj)
+      if (ids[j] >= 0 && ids[j] == ids[jj]) dup = true;
+#pragma unroll
+  for (int j = 0; j < kChunk; ++j) {
+    const int32_t s = ids[j];
+    if (s < 0) continue;
+    const double b = (pos_mask >> j) & 1u ? 1.0 : 0.0;
+    if (self_possible && s == src_row) {
+      double acc = row_dot<Row, false>(S, S, g.gmask, g.gl, dim);
+      float sc = nce_score(acc, b, lr, bad, fast);
+      update_self(S, sc, false, load_once);
+      continue;
+    }
+    Row R;
+    R.lds(slots + j * dim, g.gl);
+    double acc = row_dot<Row, false>(S, R, g.gmask, g.gl, dim);
+    float sc = nce_score(acc, b, lr, bad, fast);
+    update_pair_writeback(S, R, sc, false, atomic, Mtgt + (int64_t)s * dim, g.gl, dim);
+    if (dup) {
+#pragma unroll
+      for (int jj = j + 1; jj < kChunk; ++jj)
+        if (ids[jj] == s) R.sts(slots + jj * dim, g.gl);
+    }
+  }
+}
+
 // Batched-dot chunk (non-exact, latency variant).  With distinct sample ids
 // that all differ from the source, S before update k is
 // S + sum_{j<k} sc_j R_j, so the k-th dot is
@@ -588,7 +661,7 @@ __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &
 // the runtime-flag branches otherwise triple the unrolled code, and the
 // i-cache misses that cost show up as the top ncu stall (no_instructions).
 template <class Row, bool EXACT, int KIND, bool HOT>
-__global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : Row::kMinBlocks)
+__global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 ? 3 : Row::kMinBlocks))
     train_passes_kernel(PassArgs a) {
   constexpr int G = Row::G;
   constexpr bool BATCH = KIND == 1;
@@ -601,7 +674,51 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : Row::kMinBl
   const int64_t n = a.sources ? a.n_sources : a.V;
   if (sl.warp_base >= n) return;
   const int64_t lane_off = sl.gid - sl.warp_base;
-  if constexpr (KIND == 0) {
+  if constexpr (KIND == 3) {
+    // HOT throughput pass with the sample rows staged in shared memory
+    // (dynamic: kBlock / G groups x kChunk slots x dim floats): ~80 registers
+    // instead of 128, so 3 blocks per SM hold 1.5x the sources in flight
+    extern __shared__ float4 stage_smem[];
+    float *slots = reinterpret_cast<float *>(stage_smem) +
+                   (size_t)((threadIdx.x >> 5) * (32 / G) + (threadIdx.x & 31) / G) * kChunk * a.dim;
+    const int nsamp = 1 + a.n_neg;
+    for (int64_t p = a.pass_begin; p < a.pass_begin + a.n_passes; ++p) {
+      const int epoch = (int)(p / a.ppe);
+      const double lr = (double)__ldg(a.lr + epoch);
+      for (int64_t base = sl.warp_base; base < n; base += sl.eff) {
+        const int64_t i = base + lane_off;
+        if (!sl.enabled || i >= n) continue;
+        const int64_t v = a.sources ? (int64_t)__ldg(a.sources + i) : i;
+        const int64_t x0 = __ldg(a.xadj + v);
+        const int64_t deg = __ldg(a.xadj + v + 1) - x0;
+        if (deg == 0) continue;
+        const uint64_t key = stream_key(a.seed, a.stream, (uint64_t)p, (uint64_t)v);
+        Row S;
+        S.load(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+        bool bad_src = false;
+        for (int c0 = 0; c0 < nsamp; c0 += kChunk) {
+          int32_t ids[kChunk];
+#pragma unroll
+          for (int j = 0; j < kChunk; ++j) {
+            const int idx = c0 + j;
+            if (idx >= nsamp)
+              ids[j] = -1;
+            else if (idx == 0)
+              ids[j] = __ldg(a.adj + x0 + draw_below(key, 0, deg));
+            else
+              ids[j] = (int32_t)draw_below(key, (uint64_t)idx, a.V);
+          }
+          run_chunk_staged<Row>(S, v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, slots, g, bad_src,
+                                fast, atomic);
+        }
+        S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+        if (bad_src) {
+          bad = true;
+          first_bad = min(first_bad, epoch);
+        }
+      }
+    }
+  } else if constexpr (KIND == 0) {
     // throughput variant (full occupancy, HBM-bound): the index chain is
     // computed inline per source -- its latency hides behind other warps and
     // this keeps the kernel within 128 registers (2 blocks per SM)
@@ -816,7 +933,9 @@ __device__ __forceinline__ int64_t lower_bound_adj(const int32_t *__restrict__ a
 // gathers -- each row slot refilled with the next chunk's sample right after
 // its update, stale duplicates re-read -- measured 5.40 vs 6.32: the refill
 // loads wait on the write-back reductions still reading the slot's
-// registers; with the refill delayed by one sample, 5.14 vs 6.26.)
+// registers; with the refill delayed by one sample, 5.14 vs 6.26.  Rows
+// staged in shared memory as in the KIND 3 pass: 6.36-6.39 vs 6.24-6.26 at
+// d=128 but 2.99 vs 3.27 at d=256, not adopted.)
 //
 // Sample ids come in windows of kWin = 2 chunks: lane l of the group draws
 // flat samples l, l + G, ... of the window (the positive from the pool or the
@@ -1029,6 +1148,7 @@ struct Variant {
   // HOT instantiations (default flags fixed at compile time); null if absent
   PassFn pass_hot = nullptr;
   PassFn pass_ahead_hot = nullptr;  // KIND 2
+  PassFn pass_staged_hot = nullptr;  // KIND 3
   PassFn pass_pipe_hot = nullptr;
   PoolFn pool_hot = nullptr;       // off-diagonal pair
   PoolFn pool_hot_diag = nullptr;  // diagonal pair (Msrc == Mtgt)
@@ -1047,6 +1167,7 @@ Variant make_variant() {
   if constexpr (WITH_HOT && !EXACT) {
     v.pass_hot = train_passes_kernel<Row, false, 0, true>;
     v.pass_ahead_hot = train_passes_kernel<Row, false, 2, true>;
+    v.pass_staged_hot = train_passes_kernel<Row, false, 3, true>;
     v.pass_pipe_hot = train_passes_kernel<Row, false, 1, true>;
     v.pool_hot = train_pool_kernel<Row, false, 1>;
     v.pool_hot_diag = train_pool_kernel<Row, false, 2>;

@@ -290,13 +290,15 @@ def test_atomic_rows_keep_concurrent_updates_of_a_hot_row(cuda, orc):
     assert _rel_err(Ma[others], ref[others]) <= 1e-4
 
 
-@pytest.mark.parametrize("pipe", ["0", "1"])
+@pytest.mark.parametrize("variant", ["throughput", "latency", "staged"])
 @pytest.mark.parametrize("d", [16, 32, 64, 128, 256])
-def test_single_group_passes_match_sequential(cuda, orc, d, pipe, monkeypatch):
-    """The parallel pass kernels (throughput and latency variants) with one
-    source in flight are the reference's sequential pass up to the tree dot
-    and fp32 sigmoid: within 1e-5 relative after two passes."""
-    monkeypatch.setenv("GB_PIPE", pipe)
+def test_single_group_passes_match_sequential(cuda, orc, d, variant, monkeypatch):
+    """The parallel pass kernels (throughput, latency and shared-memory-staged
+    variants) with one source in flight are the reference's sequential pass
+    up to the tree dot and fp32 sigmoid: within 1e-5 relative after two
+    passes."""
+    monkeypatch.setenv("GB_PIPE", "1" if variant == "latency" else "0")
+    monkeypatch.setenv("GB_PASS_SMEM", "1" if variant == "staged" else "0")
     x, a = orc.rmat_graph(11, 20000, 3, densify_ids=True)
     g = Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
     M0 = orc.init_embedding(g.num_vertices, d, 1) * 20.0
