@@ -935,7 +935,9 @@ __device__ __forceinline__ int64_t lower_bound_adj(const int32_t *__restrict__ a
 // loads wait on the write-back reductions still reading the slot's
 // registers; with the refill delayed by one sample, 5.14 vs 6.26.  Rows
 // staged in shared memory as in the KIND 3 pass: 6.36-6.39 vs 6.24-6.26 at
-// d=128 but 2.99 vs 3.27 at d=256, not adopted.)
+// d=128 but 2.99 vs 3.27 at d=256; the next chunk cp.async-staged while the
+// current one trains from registers: 6.12-6.14 vs 6.27 and 3.13-3.16 vs
+// 3.25 -- neither adopted.)
 //
 // Sample ids come in windows of kWin = 2 chunks: lane l of the group draws
 // flat samples l, l + G, ... of the window (the positive from the pool or the
