@@ -313,3 +313,23 @@ def test_product_package_never_imports_the_oracle():
             src = open(os.path.join(pkg, fn)).read()
             assert not re.search(r"^\s*(from|import)\s+\S*oracle", src, re.M), fn
             assert "liboracle" not in src, fn
+
+
+def test_pair_side_pool_modes_and_balanced_config(monkeypatch):
+    """PairSides picks the pool mode from GB_POOL_MODE (compact by default,
+    materialize for deterministic runs, balanced when configured) and
+    rejects unknown modes; balanced pools need the Hogwild kernels."""
+    from paper_2008_12336_b200.bigtrain import PairSides
+    csr = (None, None)
+    st = None
+    monkeypatch.delenv("GB_POOL_MODE", raising=False)
+    assert PairSides(csr, gb.TrainConfig(), 0, 5, st).mode == "compact"
+    assert PairSides(csr, gb.TrainConfig(deterministic=True), 0, 5, st).mode == "materialize"
+    assert PairSides(csr, gb.TrainConfig(balanced_pools=True), 0, 5, st, K=4).mode == "balanced"
+    monkeypatch.setenv("GB_POOL_MODE", "fused")
+    assert PairSides(csr, gb.TrainConfig(), 0, 5, st).mode == "fused"
+    monkeypatch.setenv("GB_POOL_MODE", "bogus")
+    with pytest.raises(gb.ConfigError):
+        PairSides(csr, gb.TrainConfig(), 0, 5, st)
+    with pytest.raises(gb.ConfigError):
+        gb.TrainConfig(balanced_pools=True, deterministic=True).validate()
