@@ -210,6 +210,18 @@ def test_ragged_parts_and_tiny_levels(orc):
                             pair_fn=lambda *args: None)
 
 
+def test_virtual_streams_knob_validated(monkeypatch):
+    """GB_VIRTUAL_STREAMS accepts auto / 0 / 1 only (tournament.py)."""
+    g = Graph(4, 4, xadj=np.array([0, 1, 2, 3, 4]), adj=np.array([1, 0, 3, 2], np.int32))
+    cfg = gb.TrainConfig(dim=8, negative_samples=2, seed=5, deterministic=True)
+    monkeypatch.setenv("GB_VIRTUAL_STREAMS", "yes")
+    with pytest.raises(gb.ConfigError):
+        tn.train_tournament(g, torch.zeros(4, 8), cfg, 1, num_ranks=2,
+                            pair_fn=lambda *args: None)
+    monkeypatch.setenv("GB_VIRTUAL_STREAMS", "0")
+    tn.train_tournament(g, torch.zeros(4, 8), cfg, 1, num_ranks=2, pair_fn=lambda *args: None)
+
+
 def _nccl_worker(rank, world, port, out_path):
     import torch.distributed as dist
     from oracle import oracle as orc
