@@ -264,9 +264,10 @@ def train_tournament(g: Graph, M, cfg: TrainConfig, e_i: int, batch_size: int = 
     status = None
     # virtual ranks on one GPU: each rank's pairs go to their own stream (the
     # pairs of a round touch disjoint parts, as on G GPUs), joined once per
-    # round before the exchange.  Only small parts gain (C2: 65K-row parts
-    # 3.14 -> 5.80 G upd/s; 262K-row parts lose 10%): GB_VIRTUAL_STREAMS
-    # auto (parts under 100K rows) / 1 / 0
+    # round before the exchange.  Only small parts gain (C2, d=128: 32 MiB
+    # parts 3.14 -> 5.80 G upd/s; 64 MiB parts equal at d=128, -20% at
+    # d=256; 128 MiB parts -10%): GB_VIRTUAL_STREAMS auto (parts under
+    # 48 MiB) / 1 / 0
     streams = None
     vs = os.environ.get("GB_VIRTUAL_STREAMS", "auto")
     if vs not in ("auto", "0", "1"):
@@ -275,7 +276,7 @@ def train_tournament(g: Graph, M, cfg: TrainConfig, e_i: int, batch_size: int = 
         pair_fn, status = device_pair_fn(g, cfg, B, K)
         device = torch.device("cuda", torch.cuda.current_device())
         if not distributed and G > 1 and (
-                vs == "1" or (vs == "auto" and plan.max_rows < 100_000)):
+                vs == "1" or (vs == "auto" and plan.max_rows * d * 4 < 48 << 20)):
             streams = [torch.cuda.Stream(device) for _ in range(G)]
             rank_fns = [pair_fn] + [device_pair_fn(g, cfg, B, K, status)[0]
                                     for _ in range(G - 1)]
