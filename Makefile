@@ -3,20 +3,24 @@
 #   make lib / oracle
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
+# EXTRA / OBJDIR / LIB: A/B builds, e.g.
+#   make lib EXTRA=-DGB_SRC_DELTA=0 OBJDIR=build/ab LIB=build/ab/libgosh_b200.so
+EXTRA ?=
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
-           -Iinclude -Ipaper_2008_12336_b200/csrc --expt-relaxed-constexpr
+           -Iinclude -Ipaper_2008_12336_b200/csrc --expt-relaxed-constexpr $(EXTRA)
 PKG := paper_2008_12336_b200
 SRC := $(wildcard $(PKG)/csrc/*.cu)
-OBJ := $(patsubst $(PKG)/csrc/%.cu,build/obj/%.o,$(SRC))
+OBJDIR ?= build/obj
+OBJ := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(SRC))
 HDR := $(wildcard $(PKG)/csrc/*.cuh) include/gosh_b200.h
-LIB := $(PKG)/libgosh_b200.so
+LIB ?= $(PKG)/libgosh_b200.so
 
 all: lib oracle
 
 lib: $(LIB)
 
-build/obj/%.o: $(PKG)/csrc/%.cu $(HDR)
-	@mkdir -p build/obj
+$(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDR)
+	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(LIB): $(OBJ)

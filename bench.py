@@ -39,16 +39,14 @@ METRIC = "sample-updates/sec"
 UNIT = "updates/s"
 
 
-def workload_config(extra=None):
-    cfg = {"workload": "C2 single-level VERSE pass: R-MAT scale 20 (2^20 ids, 2^24 sampled "
-                       "edges, Graph500 a,b,c=0.57,0.19,0.19), d=128, n_neg=3",
-           "scale": SCALE, "sampled_edges": SAMPLES, "dim": DIM, "negatives": NNEG,
-           "rmat_seed": SEED, "lr": LR, "step": "one vertex pass (1 kernel launch)",
-           "kernel_flags": "default non-deterministic path (fp64 dot, fp32 sigmoid)",
-           "l2": "inputs larger than L2 (embedding matrix 512 MiB > 126 MB L2), no flush"}
-    if extra:
-        cfg.update(extra)
-    return cfg
+def workload_config():
+    """The workload keys only -- both arms print exactly this dict (the
+    driver compares them); run details go under "details"."""
+    return {"workload": "C2 single-level VERSE pass: R-MAT scale 20 (2^20 ids, 2^24 sampled "
+                        "edges, Graph500 a,b,c=0.57,0.19,0.19), d=128, n_neg=3",
+            "scale": SCALE, "sampled_edges": SAMPLES, "dim": DIM, "negatives": NNEG,
+            "rmat_seed": SEED, "lr": LR, "step": "one vertex pass (1 kernel launch)",
+            "l2": "inputs larger than L2 (embedding matrix 512 MiB > 126 MB L2), no flush"}
 
 
 def bytes_per_source(dim=DIM, n_neg=NNEG):
@@ -185,7 +183,8 @@ def run_reference(args):
         "ms_per_step": el * 1000.0 / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows / f64 dot",
         "data": "synthetic R-MAT (CPU generator, bit-identical to the GPU one)",
-        "config": workload_config({"parallelism": "host threads"}),
+        "config": workload_config(),
+        "details": {"parallelism": f"{threads} host threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{args.steps} timed full C2 passes after {args.warmup} "
                                    f"warm-up passes, oracle/gosh_oracle.c or_train_pass"},
@@ -280,6 +279,27 @@ def run_ours(args):
     e2e_value = world * e2e_upd / e2e_s
     ppe = gb.trainer.passes_per_epoch(G, cfg)
 
+    # the same pass with the reference's fp64 sigmoid (trainer.py:118) instead
+    # of the fp32 one: run-time-flag kernel, same fp64 dot and write-back
+    flags64 = _lib.GB_TRAIN_ATOMIC if (not args.store_rows) else 0
+
+    def launch64(p):
+        _lib.call("gb_train_passes", V, _lib.ptr(xadj), _lib.ptr(adj), _lib.ptr(sources),
+                  non_iso, _lib.ptr(M), DIM, NNEG, 1, 0, p, 1, 1 << 40, _lib.ptr(lrs), flags64,
+                  cap, _lib.ptr(status), stream.cuda_stream)
+
+    for p in range(3):
+        launch64(10_000 + p)
+    s64, e64 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n64 = max(3, args.steps // 2)
+    torch.cuda.synchronize()
+    s64.record(stream)
+    for p in range(n64):
+        launch64(20_000 + p)
+    e64.record(stream)
+    torch.cuda.synchronize()
+    ms64 = s64.elapsed_time(e64) / n64
+
     bps = bytes_per_source()
     achieved = non_iso * bps / (kern_ms / 1000.0) / 1e9
     peak, peak_src = measured_peak()
@@ -287,13 +307,15 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows / f64 dot",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows / f64 dot / f32 sigmoid",
         "data": "synthetic R-MAT generated on device (seeded, Graph500 parameters)",
-        "config": workload_config({
-            "vertices": V, "non_isolated_sources": non_iso, "arcs": G.num_edges,
-            "parallelism": "replicas" if world > 1 else "single GPU",
-            "inflight_groups_cap": cap, "graph_build_s": round(build_s, 3),
-            "row_writeback": "vector reductions" if (not args.store_rows) else "stores"}),
+        "config": workload_config(),
+        "details": {"vertices": V, "non_isolated_sources": non_iso, "arcs": G.num_edges,
+                    "parallelism": "replicas" if world > 1 else "single GPU",
+                    "inflight_groups_cap": cap, "graph_build_s": round(build_s, 3),
+                    "kernel_flags": "default path: fp64 dot, fp32 sigmoid, vector-reduction "
+                                    "write-back of sample rows and source-row increments",
+                    "row_writeback": "vector reductions" if (not args.store_rows) else "stores"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": non_iso * bps,
@@ -308,14 +330,117 @@ def run_ours(args):
                         f"M in/out", "steps": e2e_steps},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
+        "fp64_sigmoid": {"value": upd_per_step / (ms64 / 1000.0), "unit": UNIT,
+                         "kernel_ms": ms64, "frac": non_iso * bps / (ms64 / 1000.0) / 1e9 / peak,
+                         "note": "same pass with the reference's fp64 sigmoid/divide "
+                                 "(run-time-flag kernel) instead of the fp32 sigmoid"},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(xadj.cpu().numpy(), adj[: G.num_edges].cpu().numpy(),
                                             seconds=args.cpu_seconds)
+    del M, xadj, adj, sources
+    G = None
+    torch.cuda.empty_cache()
+    if world == 1 and not args.no_multilevel:
+        line["multilevel_c3"] = multilevel_c3(args, cpu=not args.no_cpu_baseline)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+C3_SCALE, C3_SAMPLES, C3_SEED, C3_DIM = 22, 126_000_000, 7, 128
+
+
+def multilevel_c3(args, cpu=True):
+    """The metric's second half, "embed wall time at equal AUCROC", on C3
+    (BASELINE.json configs[2]: com-orkut-shaped R-MAT, 1 GPU): the public
+    train_multilevel(host Graph) -> numpy matrix with the CLI defaults
+    (cli.py:59-78: d=128, 1000 epochs, smoothing 0.3, lr 0.035, 3 negatives,
+    vertex-pass), timed end to end -- CSR upload, coarsening, every level's
+    training, expands, the matrix download -- on the train graph of the
+    link-prediction split, then AUCROC of that embedding (device evaluator,
+    1M+1M pair subsample).  The CPU leg is the oracle's restatement of the
+    same embed on this box's host cores: the sequential coarsen_all (the
+    reference's parity path) timed whole, each level's training timed on a
+    bounded number of passes and extrapolated."""
+    import torch
+    import paper_2008_12336_b200 as gb
+    from paper_2008_12336_b200.evaluate import LinkPredictionSetup
+    t0 = time.perf_counter()
+    g = gb.rmat_graph(C3_SCALE, C3_SAMPLES, C3_SEED, densify_ids=True)
+    setup = LinkPredictionSetup.build(g, eval_seed=1, evaluator="device", eval_sample=1 << 20)
+    tg = setup.train_graph
+    xh, ah = tg.xadj, tg.adj
+    del g
+    setup_s = time.perf_counter() - t0
+    cfg = gb.TrainConfig(dim=C3_DIM, total_epochs=1000, smoothing_ratio=0.3, learning_rate=0.035,
+                         negative_samples=3, seed=1, epoch_unit="vertex-pass")
+    h = setup.hierarchy
+    plan = gb.epoch_plan(cfg.total_epochs, cfg.smoothing_ratio, h.depth).per_level
+    updates = 0
+    for i, gi in enumerate(h.graphs):
+        ppe = gb.trainer.passes_per_epoch(gi, cfg)
+        updates += int(plan[i]) * ppe * int((gi.degrees() > 0).sum()) * (1 + cfg.negative_samples)
+    runs, M = [], None
+    for _ in range(1 + args.c3_repeats):  # the first run is the warm-up
+        fresh = gb.Graph(tg.num_vertices, tg.num_edges, xadj=xh, adj=ah)  # host arrays only
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        M = gb.train_multilevel(fresh, cfg)
+        runs.append(time.perf_counter() - t1)
+        del fresh
+    embed_s = statistics.median(runs[1:])
+    auc = setup.score(M)
+    out = {"workload": "C3: R-MAT scale 22, 126M sampled edges, ids densified; link-prediction "
+                       "train graph (test fraction 0.2, eval seed 1)",
+           "vertices": tg.num_vertices, "arcs": tg.num_edges,
+           "levels": [x.num_vertices for x in h.graphs],
+           "config": "CLI defaults: d=128, 1000 epochs, smoothing 0.3, lr 0.035, n_neg 3, "
+                     "vertex-pass, seed 1",
+           "embed_s": embed_s, "embed_s_runs": runs[1:], "updates": updates,
+           "updates_per_s": updates / embed_s,
+           "h2d_bytes": int(xh.nbytes + ah.nbytes), "d2h_bytes": int(M.nbytes),
+           "aucroc": auc, "aucroc_eval": "device evaluator, 1M train + 1M test positive pairs "
+                                         "(+ as many negatives), LogRegConfig defaults",
+           "setup_s": setup_s}
+    if cpu:
+        out["cpu_baseline"] = multilevel_cpu(xh, ah, cfg, plan, seconds=args.c3_cpu_seconds)
+        out["cpu_baseline"]["speedup"] = out["cpu_baseline"]["embed_s_est"] / embed_s
+    return out
+
+
+def multilevel_cpu(xh, ah, cfg, plan, seconds=20.0):
+    from oracle import oracle as orc
+    threads = orc.max_threads()
+    t0 = time.perf_counter()
+    graphs, maps, _ = orc.coarsen_all(xh, ah, 100)
+    coarsen_s = time.perf_counter() - t0
+    per_level = max(seconds / len(graphs), 0.5)
+    train_s = 0.0
+    Mc = orc.init_embedding(len(graphs[-1][0]) - 1, cfg.dim, cfg.seed)
+    timed = 0
+    for i in range(len(graphs) - 1, -1, -1):
+        x, a = graphs[i]
+        V, E = len(x) - 1, int(x[-1])
+        passes = int(plan[i]) * orc.passes_per_epoch(V, E, cfg.epoch_unit)
+        n_run, t1 = 0, time.perf_counter()
+        while n_run < passes:
+            orc.train_pass(x, a, Mc, cfg.learning_rate, cfg.negative_samples, cfg.seed, i, n_run,
+                           nthreads=threads)
+            n_run += 1
+            if time.perf_counter() - t1 >= per_level:
+                break
+        el = time.perf_counter() - t1
+        train_s += el * passes / n_run
+        timed += n_run
+        if i > 0:
+            Mc = orc.expand(Mc, maps[i - 1][0])
+    return {"embed_s_est": coarsen_s + train_s, "coarsen_s": coarsen_s, "train_s_est": train_s,
+            "cores": threads, "kind": "port",
+            "sample": f"oracle/gosh_oracle.c: sequential coarsen_all timed whole; {timed} "
+                      f"passes timed over the {len(graphs)} levels ({threads} threads), "
+                      f"extrapolated to the plan's passes"}
 
 
 def run_tournament(args):
@@ -402,6 +527,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-multilevel", action="store_true",
+                    help="skip the C3 multilevel embed + AUCROC field")
+    ap.add_argument("--c3-repeats", type=int, default=3)
+    ap.add_argument("--c3-cpu-seconds", type=float, default=20.0)
     ap.add_argument("--workload", choices=["c2", "tournament"], default="c2")
     ap.add_argument("--dim", type=int, default=0,
                     help="tournament workload: embedding dimension (default 128; C5 uses 256)")

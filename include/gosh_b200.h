@@ -135,6 +135,14 @@ int gb_coarse_csr(int64_t num_vertices, int64_t num_edges, const int64_t *xadj,
 
 /* ---- L3: projection (trainer.py:243-249 expand_embedding) ----------------
  * out[v, :] = coarse[cmap[v], :] for v < num_rows. */
+/* Position-keyed checksum of an int32 / int64 device array (elem_bytes 4 or
+ * 8): *out = sum_i mix64((i * 0x9E3779B97F4A7C15) ^ (uint64)(int64)x[i])
+ * mod 2^64 (out is a device uint64).  Not a reference kernel: the parity
+ * check for hierarchies too large to ship as fixtures (tests compare it with
+ * the oracle's or_checksum of the reference's arrays). */
+int gb_checksum(const void *data, int64_t n, int elem_bytes, uint64_t *out,
+                void *stream_handle);
+
 int gb_expand(const float *coarse, int64_t num_clusters, int dim,
               const int32_t *cmap, int64_t num_rows, float *out,
               void *stream_handle);

@@ -66,6 +66,7 @@ def lib():
             "or_rmat_edges": (None, [_int, _i64, _dbl, _dbl, _dbl, _u64, C.c_void_p, _i64p,
                                      _i64p]),
             "or_max_threads": (_int, []),
+            "or_checksum": (_u64, [C.c_void_p, _i64, _int]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -296,3 +297,11 @@ def algorithmic_bytes_per_source(dim: int, n_neg: int) -> int:
 
 __all__ = [n for n in dir() if not n.startswith("_") and n not in ("C", "math", "np", "os",
                                                                      "subprocess")]
+
+
+def checksum(a: np.ndarray) -> int:
+    """or_checksum of an int32/int64 array (twin of the device gb_checksum)."""
+    a = np.ascontiguousarray(a)
+    if a.dtype not in (np.int32, np.int64):
+        raise TypeError("checksum takes int32 or int64 arrays")
+    return int(lib().or_checksum(a.ctypes.data, a.size, a.dtype.itemsize))

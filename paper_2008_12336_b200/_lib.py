@@ -53,6 +53,7 @@ SIGNATURES = {
     "gb_coarse_csr_workspace": (_int, [_i64, _i64, _i64, _psz]),
     "gb_coarse_csr": (_int, [_i64, _i64, _p, _p, _p, _i64, _p, _p, _pi64, _p, _sz, _p]),
     "gb_expand": (_int, [_p, _i64, _int, _p, _i64, _p, _p]),
+    "gb_checksum": (_int, [_p, _i64, _int, _p, _p]),
     "gb_train_passes": (_int, [_i64, _p, _p, _p, _i64, _p, _int, _int, _u64, _u64, _i64, _i64,
                                _i64, _p, C.c_uint, _i64, _p, _p]),
     "gb_active_sources_workspace": (_int, [_i64, _psz]),

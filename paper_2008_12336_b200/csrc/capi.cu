@@ -47,15 +47,29 @@ GB_API int gb_device_info(int device, int *num_sms, int *max_warps_per_sm) {
   return GB_OK;
 }
 
+// Failure is an expected outcome here (already pinned / registered memory,
+// some mappings): callers fall back to a pinned copy.  The runtime's sticky
+// last-error slot is cleared so the failure cannot surface in the next
+// launch's GB_CHECK_LAUNCH (cudaGetLastError) as an unrelated error.
 GB_API int gb_host_register(void *ptr, size_t bytes) {
   GB_REQUIRE(ptr && bytes > 0, "gb_host_register: bad args");
-  GB_CUDA_TRY(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+  const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterDefault);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    gb::set_error("cudaHostRegister: %s", cudaGetErrorString(e));
+    return GB_E_CUDA;
+  }
   return GB_OK;
 }
 
 GB_API int gb_host_unregister(void *ptr) {
   GB_REQUIRE(ptr, "gb_host_unregister: null pointer");
-  GB_CUDA_TRY(cudaHostUnregister(ptr));
+  const cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    gb::set_error("cudaHostUnregister: %s", cudaGetErrorString(e));
+    return GB_E_CUDA;
+  }
   return GB_OK;
 }
 

@@ -752,6 +752,24 @@ GB_API int gb_expand(const float *coarse, int64_t num_clusters, int dim, const i
   return GB_OK;
 }
 
+// Position-keyed checksum of an integer array: sum over i of
+// mix64((i * GOLDEN) ^ (uint64)(int64)x[i]) mod 2^64 (elements sign-extended
+// to 64 bits).  Order-sensitive through the index, associative through the
+// sum, so it is one HBM pass; the oracle (or_checksum) computes the same
+// number on the host.  Used to compare hierarchies whose arrays are too big
+// to ship as fixtures (config-scale coarsening parity).
+template <typename T>
+__global__ void checksum_kernel(const T *__restrict__ x, int64_t n,
+                                unsigned long long *__restrict__ out) {
+  uint64_t acc = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc += mix64(((uint64_t)i * kGolden) ^ (uint64_t)(int64_t)__ldg(x + i));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)acc);
+}
+
 static int active_layout(Carver &c, int64_t V, int32_t **ids, char **flag, int64_t **cnt,
                          void **tmp, size_t *tb) {
   *ids = c.take<int32_t>(V);
@@ -800,5 +818,22 @@ GB_API int gb_active_sources(int64_t num_vertices, const int64_t *xadj, int32_t 
   GB_CUDA_TRY(cudaMemcpyAsync(&n, cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GB_CUDA_TRY(cudaStreamSynchronize(st));
   *count_out = n;
+  return GB_OK;
+}
+
+GB_API int gb_checksum(const void *data, int64_t n, int elem_bytes, uint64_t *out,
+                       void *stream_handle) {
+  GB_REQUIRE(out && n >= 0 && (n == 0 || data), "gb_checksum: bad args");
+  GB_REQUIRE(elem_bytes == 4 || elem_bytes == 8, "gb_checksum: elem_bytes must be 4 or 8");
+  cudaStream_t st = as_stream(stream_handle);
+  GB_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(uint64_t), st));
+  if (n == 0) return GB_OK;
+  const int grid = (int)std::min<int64_t>(blocks_for(n), (int64_t)num_sms() * 8);
+  auto *o = reinterpret_cast<unsigned long long *>(out);
+  if (elem_bytes == 4)
+    checksum_kernel<<<grid, 256, 0, st>>>(static_cast<const int32_t *>(data), n, o);
+  else
+    checksum_kernel<<<grid, 256, 0, st>>>(static_cast<const int64_t *>(data), n, o);
+  GB_CHECK_LAUNCH();
   return GB_OK;
 }

@@ -111,9 +111,15 @@ void select_hot(Variant &v, unsigned flags, bool diagonal, bool pool_materialize
   if (p && (pool_materialized || pool_balanced)) v.pool = p;
 }
 
+// Dynamic shared memory of a KIND 0/2 pass or pair-side launch: one slot per
+// group for the source's initial copy (SrcKeep) on vector layouts.
+size_t s0_bytes(const Variant &var, int dim) {
+  return var.s0_smem ? (size_t)(kBlock / var.G) * dim * sizeof(float) : 0;
+}
+
 // Launch of a pair-side kernel.
 int launch_pool(const Variant &var, const PoolArgs &a, int grid, cudaStream_t st) {
-  var.pool<<<grid, kBlock, 0, st>>>(a);
+  var.pool<<<grid, kBlock, s0_bytes(var, a.dim), st>>>(a);
   GB_CHECK_LAUNCH();
   return GB_OK;
 }
@@ -122,9 +128,10 @@ bool aligned16(const void *p, int dim) {
   return (reinterpret_cast<uintptr_t>(p) & 15u) == 0 && dim % 4 == 0;
 }
 
-int grid_for(const void *sym, int G, int64_t max_groups, int64_t work_items, int *grid) {
+int grid_for(const void *sym, int G, int64_t max_groups, int64_t work_items, int *grid,
+             size_t smem = 0) {
   int occ = 0;
-  GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym, kBlock, 0));
+  GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym, kBlock, smem));
   if (occ < 1) occ = 1;
   const int64_t groups_per_block = kBlock / G;
   const int64_t want = (int64_t)num_sms() * occ;
@@ -162,11 +169,11 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
              passes_per_epoch, lr_per_epoch, (flags & GB_TRAIN_REUSE) != 0,
              (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status};
   int grid = 1, block = kBlock;
-  size_t smem = 0;
+  size_t smem = s0_bytes(var, dim);
   PassFn fn = var.pass;
   if (!exact) {
     const int64_t items = sources ? n_sources : num_vertices;
-    int rc = grid_for((const void *)var.pass, var.G, max_groups, items, &grid);
+    int rc = grid_for((const void *)var.pass, var.G, max_groups, items, &grid, smem);
     if (rc) return rc;
     // Uncapped launches (the cap reaches the throughput variant's full
     // occupancy) run KIND 3: sample rows staged in shared memory by cp.async,
@@ -177,7 +184,7 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
     {
       int occ0 = 0;
       GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, (const void *)var.pass,
-                                                                kBlock, 0));
+                                                                kBlock, smem));
       const int64_t full0 = (int64_t)num_sms() * std::max(occ0, 1) * (kBlock / var.G);
       const int64_t want = std::min<int64_t>(max_groups > 0 ? max_groups : INT64_MAX, items);
       const char *env = std::getenv("GB_PASS_SMEM");
@@ -205,7 +212,7 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
     // fits its capacity.  GB_PIPE=0/1 forces the choice for experiments.
     int occ = 0;
     GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)var.pass,
-                                                              kBlock, 0));
+                                                              kBlock, smem));
     const int64_t full = (int64_t)num_sms() * std::max(occ, 1) * (kBlock / var.G);
     const int64_t groups = std::min<int64_t>(max_groups > 0 ? max_groups : INT64_MAX, items);
     Variant lat;
@@ -261,7 +268,7 @@ GB_API int gb_train_pool_side(float *Msrc, float *Mtgt, int dim, const int32_t *
              (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status};
   int grid = 1;
   if (!exact) {
-    int rc = grid_for((const void *)var.pool, var.G, max_groups, n_src, &grid);
+    int rc = grid_for((const void *)var.pool, var.G, max_groups, n_src, &grid, s0_bytes(var, dim));
     if (rc) return rc;
   }
   return launch_pool(var, a, grid, as_stream(stream_handle));
@@ -288,7 +295,7 @@ GB_API int gb_train_pool_list(float *Msrc, float *Mtgt, int dim, const int32_t *
              exact ? 1 : max_groups, status};
   int grid = 1;
   if (!exact) {
-    int rc = grid_for((const void *)var.pool, var.G, max_groups, max_src, &grid);
+    int rc = grid_for((const void *)var.pool, var.G, max_groups, max_src, &grid, s0_bytes(var, dim));
     if (rc) return rc;
   }
   return launch_pool(var, a, grid, as_stream(stream_handle));
@@ -317,7 +324,7 @@ GB_API int gb_train_pool_balanced(float *Msrc, float *Mtgt, int dim, const int32
              !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status};
   int grid = 1;
   if (!exact) {
-    int rc = grid_for((const void *)var.pool, var.G, max_groups, max_src, &grid);
+    int rc = grid_for((const void *)var.pool, var.G, max_groups, max_src, &grid, s0_bytes(var, dim));
     if (rc) return rc;
   }
   return launch_pool(var, a, grid, as_stream(stream_handle));

@@ -111,6 +111,19 @@ struct VecRow {
                  "f"(d[1]), "f"(d[2]), "f"(d[3])
                  : "memory");
   }
+  // source-row write-back against the initial copy kept in a shared slot
+  // (see SrcKeep): the increments x - s0 are added by vector reductions
+  __device__ __forceinline__ void red_delta_slot(float *row, const float *s0, int gl) const {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const float4 o = reinterpret_cast<const float4 *>(s0)[k * G + gl];
+      float *p = row + 4 * (k * G + gl);
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p),
+                   "f"(__fsub_rn(x[4 * k + 0], o.x)), "f"(__fsub_rn(x[4 * k + 1], o.y)),
+                   "f"(__fsub_rn(x[4 * k + 2], o.z)), "f"(__fsub_rn(x[4 * k + 3], o.w))
+                   : "memory");
+    }
+  }
   // Serial dot in ascending element order (the reference's loop order,
   // trainer.py:122-123): element t = 4*(k*G + l) + c.
   __device__ __forceinline__ static double serial_dot(const VecRow &a, const VecRow &b,
@@ -149,6 +162,7 @@ struct ScalarRow {
     for (int k = 0; k < NS; ++k)
       if (valid(k, gl, dim)) __stcg(row + k * 32 + gl, x[k]);
   }
+  static constexpr bool kStageable = false;
   static constexpr int kRedWidth = 1;
   __device__ __forceinline__ static void red_part(float *row, int gl, int dim, int k,
                                                   const float (&d)[1]) {
@@ -277,6 +291,81 @@ __device__ __forceinline__ void update_pair_writeback(Row &S, Row &R, float sc, 
   }
 }
 
+// Source-row write-back.  Plain store (EXACT kernels, atomic off): the row
+// trained in registers replaces the stored one.  atomic: the source's own
+// increments S - S0 (S0 = the row as loaded) are added with vector
+// reductions instead, so increments other groups reduced into this row while
+// it trained (the source is also their sample -- hub rows are everybody's
+// positive) are kept rather than overwritten by the store; the reference's
+// per-element read-modify-write (trainer.py:131-140) loses at most one
+// element's worth.  Uncontended this gives fl(S0 + fl(S - S0)), which is S
+// whenever S0 and S are within a factor 2 (Sterbenz) and within an ulp of
+// max(|S|,|S0|) otherwise.
+#ifndef GB_SRC_DELTA
+#define GB_SRC_DELTA 1  // 0: plain source-row stores also with atomic write-back (A/B builds)
+#endif
+template <class Row>
+__device__ __forceinline__ void writeback_source(const Row &S, const Row &S0, float *row, int gl,
+                                                 int dim, bool atomic) {
+  if (!atomic || !GB_SRC_DELTA) {
+    S.store(row, gl, dim);
+    return;
+  }
+  constexpr int W = Row::kRedWidth;
+#pragma unroll
+  for (int k0 = 0; k0 < Row::E; k0 += W) {
+    float d[W];
+#pragma unroll
+    for (int c = 0; c < W; ++c) d[c] = __fsub_rn(S.x[k0 + c], S0.x[k0 + c]);
+    Row::red_part(row, gl, dim, k0, d);
+  }
+}
+
+// Where a source row's initial copy S0 lives while the group trains it.
+// Registers (any layout): 4*NV more live registers per lane -- at d=128 that
+// pushed the 2-3 blocks/SM kernels into 80-120 bytes of spills and cost the
+// C2 pass 19% (4.33 vs 5.32 G upd/s).  Shared slot (vector layouts): the
+// group's lanes store their own float4 pieces of S0 (no cross-lane traffic,
+// so no barrier) and read them back for the write-back.
+template <class Row, bool SMEM>
+struct SrcKeep;
+
+template <class Row>
+struct SrcKeep<Row, false> {
+  Row S0;
+  __device__ __forceinline__ explicit SrcKeep(float *) {}
+  __device__ __forceinline__ void save(const Row &S, int) { S0 = S; }
+  __device__ __forceinline__ void writeback(const Row &S, float *row, int gl, int dim,
+                                            bool atomic) const {
+    writeback_source(S, S0, row, gl, dim, atomic);
+  }
+};
+
+template <class Row>
+struct SrcKeep<Row, true> {
+  float *slot;
+  __device__ __forceinline__ explicit SrcKeep(float *s) : slot(s) {}
+  __device__ __forceinline__ void save(const Row &S, int gl) {
+    if (GB_SRC_DELTA) S.sts(slot, gl);
+  }
+  __device__ __forceinline__ void writeback(const Row &S, float *row, int gl, int dim,
+                                            bool atomic) const {
+    if (atomic && GB_SRC_DELTA)
+      S.red_delta_slot(row, slot, gl);
+    else
+      S.store(row, gl, dim);
+  }
+};
+
+// The calling group's base in the kernel's dynamic shared memory, `per`
+// floats per group.
+template <class Row>
+__device__ __forceinline__ float *group_smem(int per) {
+  extern __shared__ float4 gb_dyn_smem[];
+  return reinterpret_cast<float *>(gb_dyn_smem) +
+         (size_t)((threadIdx.x >> 5) * (32 / Row::G) + (threadIdx.x & 31) / Row::G) * per;
+}
+
 // Self-sample (s == v).  In-place rule of the single-array kernel
 // (_train_pass passes M twice): M[v] = fl(fl(vo + vo*sc) + vo*sc).  Load-once
 // rule of the two-array pool kernel on a diagonal pair (numba marks the two
@@ -385,7 +474,11 @@ __device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t
 }
 
 // run_chunk with the sample rows staged in the group's shared slots (KIND 3,
-// vector layouts only): only the row being trained occupies registers.
+// vector layouts only): slot 0 holds the source's initial copy (SrcKeep),
+// samples 1..3 of the chunk are cp.async-staged into slots 1..3 (no
+// registers held while in flight) and come to registers one at a time when
+// they train; sample 0 (the positive, whose address arrives last through the
+// xadj -> adj chain) is loaded straight into registers.
 template <class Row>
 __device__ __forceinline__ void run_chunk_staged(Row &S, int64_t src_row,
                                                  const int32_t (&ids)[kChunk], unsigned pos_mask,
@@ -394,10 +487,14 @@ __device__ __forceinline__ void run_chunk_staged(Row &S, int64_t src_row,
                                                  bool fast, bool atomic, bool self_possible = true,
                                                  bool load_once = false) {
 #pragma unroll
-  for (int j = 0; j < kChunk; ++j)
+  for (int j = 1; j < kChunk; ++j)
     if (ids[j] >= 0 && !(self_possible && ids[j] == src_row))
       Row::stage(slots + j * dim, Mtgt + (int64_t)ids[j] * dim, g.gl);
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  Row R;
+  if (ids[0] >= 0 && !(self_possible && ids[0] == src_row))
+    R.load(Mtgt + (int64_t)ids[0] * dim, g.gl, dim);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   bool dup = false;
 #pragma unroll
   for (int j = 0; j < kChunk; ++j)
@@ -415,8 +512,7 @@ __device__ __forceinline__ void run_chunk_staged(Row &S, int64_t src_row,
       update_self(S, sc, false, load_once);
       continue;
     }
-    Row R;
-    R.lds(slots + j * dim, g.gl);
+    if (j > 0) R.lds(slots + j * dim, g.gl);
     double acc = row_dot<Row, false>(S, R, g.gmask, g.gl, dim);
     float sc = nce_score(acc, b, lr, bad, fast);
     update_pair_writeback(S, R, sc, false, atomic, Mtgt + (int64_t)s * dim, g.gl, dim);
@@ -620,6 +716,7 @@ __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &
   const double lr = (double)d.lr;
   Row S;
   S.load(a.M + (int64_t)d.v * a.dim, g.gl, a.dim);
+  const Row S0 = S;
   bool bad_src = false;
   if constexpr (BATCH) {
     if (EXACT ||
@@ -638,7 +735,7 @@ __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &
     run_chunk<Row, EXACT>(S, d.v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, reuse, true, false, g,
                           bad_src, fast, atomic);
   }
-  S.store(a.M + (int64_t)d.v * a.dim, g.gl, a.dim);
+  writeback_source(S, S0, a.M + (int64_t)d.v * a.dim, g.gl, a.dim, atomic && !EXACT);
   if (bad_src) {
     bad = true;
     first_bad = min(first_bad, d.epoch);
@@ -665,6 +762,9 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 
     train_passes_kernel(PassArgs a) {
   constexpr int G = Row::G;
   constexpr bool BATCH = KIND == 1;
+  // KIND 0 / 2 keep the source's initial copy in a shared slot per group
+  // (launched with kBlock / G * dim floats of dynamic shared memory)
+  constexpr bool kS0Smem = Row::kStageable && !EXACT;
   const bool fast = HOT || a.fast, atomic = HOT || a.atomic, reuse = !HOT && a.reuse;
   const GroupCtx g = group_ctx<Row>();
   const Slots<Row> sl(a.max_groups);
@@ -678,9 +778,8 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 
     // HOT throughput pass with the sample rows staged in shared memory
     // (dynamic: kBlock / G groups x kChunk slots x dim floats): ~80 registers
     // instead of 128, so 3 blocks per SM hold 1.5x the sources in flight
-    extern __shared__ float4 stage_smem[];
-    float *slots = reinterpret_cast<float *>(stage_smem) +
-                   (size_t)((threadIdx.x >> 5) * (32 / G) + (threadIdx.x & 31) / G) * kChunk * a.dim;
+    float *slots = group_smem<Row>(kChunk * a.dim);
+    SrcKeep<Row, true> keep(slots);  // slot 0
     const int nsamp = 1 + a.n_neg;
     for (int64_t p = a.pass_begin; p < a.pass_begin + a.n_passes; ++p) {
       const int epoch = (int)(p / a.ppe);
@@ -695,6 +794,7 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 
         const uint64_t key = stream_key(a.seed, a.stream, (uint64_t)p, (uint64_t)v);
         Row S;
         S.load(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+        keep.save(S, g.gl);
         bool bad_src = false;
         for (int c0 = 0; c0 < nsamp; c0 += kChunk) {
           int32_t ids[kChunk];
@@ -711,7 +811,7 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 
           run_chunk_staged<Row>(S, v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, slots, g, bad_src,
                                 fast, atomic);
         }
-        S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+        keep.writeback(S, a.M + v * (int64_t)a.dim, g.gl, a.dim, atomic && !EXACT);
         if (bad_src) {
           bad = true;
           first_bad = min(first_bad, epoch);
@@ -723,6 +823,7 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 
     // computed inline per source -- its latency hides behind other warps and
     // this keeps the kernel within 128 registers (2 blocks per SM)
     const int nsamp = 1 + a.n_neg;
+    SrcKeep<Row, kS0Smem> keep(kS0Smem ? group_smem<Row>(a.dim) : nullptr);
     for (int64_t p = a.pass_begin; p < a.pass_begin + a.n_passes; ++p) {
       const int epoch = (int)(p / a.ppe);
       const double lr = (double)__ldg(a.lr + epoch);
@@ -736,6 +837,7 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 
         const uint64_t key = stream_key(a.seed, a.stream, (uint64_t)p, (uint64_t)v);
         Row S;
         S.load(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+        keep.save(S, g.gl);
         bool bad_src = false;
         for (int c0 = 0; c0 < nsamp; c0 += kChunk) {
           int32_t ids[kChunk];
@@ -752,7 +854,7 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 
           run_chunk<Row, EXACT>(S, v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, reuse, true, false,
                                 g, bad_src, fast, atomic);
         }
-        S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+        keep.writeback(S, a.M + v * (int64_t)a.dim, g.gl, a.dim, atomic && !EXACT);
         if (bad_src) {
           bad = true;
           first_bad = min(first_bad, epoch);
@@ -768,6 +870,7 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 
     // GB_PASS_AHEAD=1; deeper index pipelines spill at 128 registers, and
     // lane-batched source id loads measured 4.95)
     const int nsamp = 1 + a.n_neg;
+    SrcKeep<Row, kS0Smem> keep(kS0Smem ? group_smem<Row>(a.dim) : nullptr);
     const int64_t spp = (n - sl.warp_base + sl.eff - 1) / sl.eff;  // steps per pass
     const int64_t total = spp * a.n_passes;
     // step cursor (uniform across the warp): pass p, item base
@@ -822,6 +925,7 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 
       const int64_t v = cur.v;
       Row S;
       S.load(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+      keep.save(S, g.gl);
       int32_t ids[kChunk];
 #pragma unroll
       for (int j = 0; j < kChunk; ++j)  // negatives: uniform over V (trainer.py:205-206)
@@ -842,7 +946,7 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 
         compute_chunk<Row, EXACT>(S, R, v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, reuse, true,
                                   false, g, bad_src, fast, atomic);
       }
-      S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+      keep.writeback(S, a.M + v * (int64_t)a.dim, g.gl, a.dim, atomic && !EXACT);
       if (bad_src) {
         bad = true;
         first_bad = min(first_bad, cur.epoch);
@@ -947,6 +1051,9 @@ template <class Row, bool EXACT, int MODE>
 __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_pool_kernel(PoolArgs a) {
   constexpr int G = Row::G;
   constexpr int kWin = 2 * kChunk;
+  // the source's initial copy in a shared slot per group (kBlock / G * dim
+  // floats of dynamic shared memory), as in train_passes_kernel
+  constexpr bool kS0Smem = Row::kStageable && !EXACT;
   constexpr int PL = (kWin + G - 1) / G;  // window samples per lane
   const GroupCtx g = group_ctx<Row>();
   const Slots<Row> sl(a.max_groups);
@@ -992,6 +1099,7 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
     }
     const uint64_t key = stream_key(a.seed, a.side, 1, (uint64_t)i);
     Row S;
+    SrcKeep<Row, kS0Smem> keep(kS0Smem ? group_smem<Row>(a.dim) : nullptr);
     bool loaded = false;
     // lane's samples of window c0 (ids, -1 = none) and the window's positive
     // bits.  (An L2 prefetch of the next window's rows was measured and
@@ -1059,6 +1167,7 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
         if (!(ids[0] >= 0 || ids[1] >= 0 || ids[2] >= 0 || ids[3] >= 0)) continue;
         if (!loaded) {
           S.load(a.Msrc + i * (int64_t)a.dim, g.gl, a.dim);
+          keep.save(S, g.gl);
           loaded = true;
         }
         const unsigned pos_mask = (wpos_cur >> (h * kChunk)) & ((1u << kChunk) - 1u);
@@ -1069,7 +1178,7 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
                               bad, fast, atomic);
       }
     }
-    if (loaded) S.store(a.Msrc + i * (int64_t)a.dim, g.gl, a.dim);
+    if (loaded) keep.writeback(S, a.Msrc + i * (int64_t)a.dim, g.gl, a.dim, atomic && !EXACT);
   }
   if (g.gl == 0) {
     if (pos_count) atomicAdd(reinterpret_cast<unsigned long long *>(a.status + 2), pos_count);
@@ -1114,6 +1223,7 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) apply_lis
     const int64_t v = a.src[i];
     Row S;
     S.load(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+    const Row S0 = S;
     for (int c0 = 0; c0 < a.k; c0 += kChunk) {
       int32_t ids[kChunk];
       unsigned pos_mask = 0;
@@ -1126,7 +1236,7 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) apply_lis
       run_chunk<Row, EXACT>(S, v, ids, pos_mask, a.M, a.dim, a.lr, a.reuse, true, false, g, bad,
                             a.fast, a.atomic);
     }
-    S.store(a.M + v * (int64_t)a.dim, g.gl, a.dim);
+    writeback_source(S, S0, a.M + v * (int64_t)a.dim, g.gl, a.dim, a.atomic && !EXACT);
   }
   if (bad && g.gl == 0) {
     atomicOr(reinterpret_cast<unsigned long long *>(a.status), 1ull);
@@ -1143,6 +1253,7 @@ using ListFn = void (*)(ListArgs);
 
 struct Variant {
   int G = 0;
+  bool s0_smem = false;  // pass KIND 0/2 and pool kernels take kBlock/G*dim floats of smem
   PassFn pass = nullptr;       // throughput (full occupancy)
   PassFn pass_pipe = nullptr;  // latency (capped launches)
   PoolFn pool = nullptr;
@@ -1162,6 +1273,7 @@ template <class Row, bool EXACT, bool WITH_HOT = false>
 Variant make_variant() {
   Variant v;
   v.G = Row::G;
+  v.s0_smem = Row::kStageable && !EXACT;
   v.pass = train_passes_kernel<Row, EXACT, 0, false>;
   v.pass_pipe = train_passes_kernel<Row, EXACT, 1, false>;
   v.pool = train_pool_kernel<Row, EXACT, 0>;

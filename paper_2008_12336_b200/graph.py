@@ -198,6 +198,22 @@ def _csr_device(num_vertices: int, src: torch.Tensor, dst: torch.Tensor, flags: 
                  adj_dev=adj)
 
 
+def array_checksum(t) -> int:
+    """Position-keyed checksum of an int32/int64 array on the device
+    (gb_checksum): sum_i mix64((i * 0x9E3779B97F4A7C15) ^ int64(x[i])) mod
+    2^64 -- the oracle's or_checksum of the same array.  Compares
+    config-scale hierarchies against the reference without moving GBs."""
+    if not isinstance(t, torch.Tensor):
+        t = torch.from_numpy(np.ascontiguousarray(t))
+    if t.dtype not in (torch.int32, torch.int64):
+        raise TypeError("array_checksum takes int32 or int64 arrays")
+    t = t.cuda().contiguous()
+    out = torch.zeros(1, dtype=torch.int64, device=t.device)
+    _lib.call("gb_checksum", _lib.ptr(t), t.numel(), t.element_size(), _lib.ptr(out),
+              _lib.stream())
+    return int(out.item()) & 0xFFFFFFFFFFFFFFFF
+
+
 def from_edges(pairs: Iterable[tuple[int, int]] | np.ndarray, num_vertices: int | None = None,
                directed: bool = False) -> Graph:
     """CSR from (u, v) pairs over dense ids: self-loops and duplicate arcs

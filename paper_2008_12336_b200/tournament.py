@@ -431,7 +431,9 @@ def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
     if hierarchy is None:
         hierarchy = coarsen_all(g0, threshold=threshold)
     depth = hierarchy.depth
-    plan = epoch_plan(cfg.total_epochs, cfg.smoothing_ratio, depth).per_level
+    # total_epochs == 0: the random-projection baseline, like train_multilevel
+    plan = (np.zeros(depth, dtype=np.int64) if cfg.total_epochs == 0
+            else epoch_plan(cfg.total_epochs, cfg.smoothing_ratio, depth).per_level)
     _lib.require_cuda()
     M = torch.from_numpy(init_embedding(hierarchy.graphs[-1].num_vertices, cfg.dim,
                                         cfg.seed)).cuda()
@@ -443,7 +445,7 @@ def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
         sharded = i < shard_levels and g_i.num_vertices >= 2 * (
             dist.get_world_size(group) if distributed else (num_ranks or 1))
         t0 = time.perf_counter()
-        if sharded:
+        if sharded and e_i > 0:
             if distributed and not broadcast_done:
                 dist.broadcast(M, 0, group=group)
                 broadcast_done = True

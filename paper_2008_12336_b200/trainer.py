@@ -183,12 +183,14 @@ def update_embedding(M, v: int, s: int, b: int, lr: float,
     _lib.require_cuda()
     flags = _lib.GB_TRAIN_EXACT | (_lib.GB_TRAIN_REUSE if reuse_updated_source else 0)
     status = _lib.new_status()
+    dm = None
     if isinstance(M, np.ndarray):
         rows = [v] if v == s else [v, s]
         buf = torch.from_numpy(np.ascontiguousarray(M[rows])).cuda()
         lv, ls = 0, (0 if v == s else 1)
-    else:
-        buf, lv, ls = _DeviceMatrix(M).dev, v, s
+    else:  # CUDA tensor: in place; host tensor: staged and written back by close()
+        dm = _DeviceMatrix(M)
+        buf, lv, ls = dm.dev, v, s
     src = torch.tensor([lv], dtype=torch.int64, device="cuda")
     smp = torch.tensor([ls], dtype=torch.int64, device="cuda")
     lab = torch.tensor([1 if b else 0], dtype=torch.int8, device="cuda")
@@ -197,6 +199,8 @@ def update_embedding(M, v: int, s: int, b: int, lr: float,
               _lib.stream())
     if isinstance(M, np.ndarray):
         M[rows] = buf.cpu().numpy()
+    else:
+        dm.close()
 
 
 def apply_sample_lists(M, sources, samples, labels, lr: float, deterministic: bool = False,

@@ -31,7 +31,23 @@ out = {"graph": {"scale": 14, "samples": 262144, "seed": 7, "densified": True,
                     "learning_rate": 0.035, "dim": 32, "negative_samples": 3,
                     "epoch_unit": "edge-scaled", "eval_seed": 1, "num_workers": 1},
        "runs": []}
-seeds = [int(s) for s in sys.argv[1:]] or [1, 2, 3, 4, 5]
+# usage: c1_reference_auc.py [--out PATH] [seed ...]; several processes may
+# run disjoint seed sets into separate files, merged by --merge
+args = sys.argv[1:]
+out_path = os.path.join(ROOT, "tests", "golden", "c1_reference_auc.json")
+if args[:1] == ["--merge"]:
+    runs = []
+    for p in args[1:]:
+        with open(p) as f:
+            runs += json.load(f)["runs"]
+    out["runs"] = sorted({r["seed"]: r for r in runs}.values(), key=lambda r: r["seed"])
+    args = []
+    seeds = []
+elif args[:1] == ["--out"]:
+    out_path, args = args[1], args[2:]
+    seeds = [int(s) for s in args] or [1, 2, 3, 4, 5]
+else:
+    seeds = [int(s) for s in args] or [1, 2, 3, 4, 5]
 for seed in seeds:
     cfg = ml.TrainConfig(dim=32, total_epochs=1000, smoothing_ratio=0.3, learning_rate=0.035,
                          negative_samples=3, seed=seed, num_workers=1,
@@ -44,6 +60,6 @@ for seed in seeds:
 aucs = [r["aucroc"] for r in out["runs"]]
 out["mean"] = float(np.mean(aucs))
 out["std"] = float(np.std(aucs))
-with open(os.path.join(ROOT, "tests", "golden", "c1_reference_auc.json"), "w") as f:
+with open(out_path, "w") as f:
     json.dump(out, f, indent=1)
 print("mean", out["mean"], "std", out["std"])

@@ -1,0 +1,93 @@
+"""Parity at BASELINE.json's config scale (GPU box).
+
+* Coarsening of the C3-shaped graph (R-MAT scale 22, 126M samples, ids
+  densified: 2.73M vertices, 236M arcs) equals the REFERENCE's
+  coarsen_all(num_workers=1) level by level: vertex/arc/cluster counts and
+  position-keyed checksums of xadj, adj and map (tests/golden/
+  coarsen_c3_hashes.json, made by make_coarsen_hashes.py from mlembed; the
+  oracle's hierarchy is identical).  The device computes the checksums
+  (gb_checksum), so no GB-sized array leaves HBM.
+
+* Link-prediction AUCROC on C1 (the north star's third bar: within 0.01 of
+  the reference end to end).  Protocol of tests/golden/c1_reference_auc.json
+  (normal preset, d=32, edge-scaled, eval seed 1; the reference at
+  num_workers=1 for training seeds 1..30): the default Hogwild path trains
+  the same 30 seeds on the same split and hierarchy, the device evaluator
+  scores them, and the paired differences (same seed) must have |mean| <=
+  0.01 with the 95% t-interval inside +-0.01; the unpaired mean too.
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2008_12336_b200 as gb
+from paper_2008_12336_b200.evaluate import LinkPredictionSetup, aucroc_parity_interval
+from paper_2008_12336_b200.graph import array_checksum
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+AUC_TOL = 0.01
+
+
+def test_c3_coarsening_matches_reference_checksums(cuda):
+    with open(os.path.join(GOLDEN, "coarsen_c3_hashes.json")) as f:
+        gold = json.load(f)
+    gg = gold["graph"]
+    g = gb.rmat_graph(gg["scale"], gg["samples"], gg["seed"], densify_ids=True)
+    h = gb.coarsen_all(g, threshold=gold["threshold"])
+    assert h.depth == gold["depth"] and bool(h.stalled) == gold["stalled"]
+    for L, want in enumerate(gold["levels"]):
+        gl = h.graphs[L]
+        x, a = gl.device_csr()
+        assert (gl.num_vertices, gl.num_edges) == (want["vertices"], want["arcs"]), L
+        assert str(array_checksum(x)) == want["xadj"], ("xadj", L)
+        assert str(array_checksum(a[: gl.num_edges])) == want["adj"], ("adj", L)
+        if "map" in want:
+            m = h.mappings[L]
+            assert m.num_clusters == want["clusters"], L
+            assert str(array_checksum(m.device_map())) == want["map"], ("map", L)
+
+
+def test_checksum_matches_oracle(cuda, orc):
+    rng = np.random.default_rng(3)
+    for dt in (np.int32, np.int64):
+        x = rng.integers(-2**31, 2**31 - 1, size=100_003).astype(dt)
+        assert array_checksum(x) == orc.checksum(x)
+    assert array_checksum(np.zeros(0, dtype=np.int32)) == 0
+
+
+def _c1_setup():
+    with open(os.path.join(GOLDEN, "c1_reference_auc.json")) as f:
+        ref = json.load(f)
+    gp, pr = ref["graph"], ref["protocol"]
+    g = gb.rmat_graph(gp["scale"], gp["samples"], gp["seed"], densify_ids=gp["densified"])
+    assert (g.num_vertices, g.num_edges) == (gp["vertices"], gp["arcs"])
+    setup = LinkPredictionSetup.build(g, eval_seed=pr["eval_seed"], evaluator="device")
+    # the split/train graph are the reference's (its counts are in the fixture)
+    assert setup.counts == ref["runs"][0]["counts"]
+    return ref, pr, setup
+
+
+def test_c1_aucroc_parity_with_reference(cuda):
+    ref, pr, setup = _c1_setup()
+    runs = {r["seed"]: r["aucroc"] for r in ref["runs"]}
+    seeds = sorted(runs)
+    assert len(seeds) >= 20
+    mine = []
+    for seed in seeds:
+        cfg = gb.TrainConfig(dim=pr["dim"], total_epochs=pr["total_epochs"],
+                             smoothing_ratio=pr["smoothing_ratio"],
+                             learning_rate=pr["learning_rate"],
+                             negative_samples=pr["negative_samples"], seed=seed,
+                             epoch_unit=pr["epoch_unit"])
+        mine.append(setup.score(setup.embed(cfg)))
+    diffs = np.array(mine) - np.array([runs[s] for s in seeds])
+    ci = aucroc_parity_interval(diffs)
+    msg = f"paired diff {ci}, ours {np.mean(mine):.4f} vs reference {np.mean(list(runs.values())):.4f}"
+    assert abs(ci["mean"]) <= AUC_TOL, msg
+    assert -AUC_TOL <= ci["lo"] and ci["hi"] <= AUC_TOL, msg
+    assert abs(np.mean(mine) - np.mean([runs[s] for s in seeds])) <= AUC_TOL, msg
