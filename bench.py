@@ -343,6 +343,12 @@ def run_ours(args):
     torch.cuda.empty_cache()
     if world == 1 and not args.no_multilevel:
         line["multilevel_c3"] = multilevel_c3(args, cpu=not args.no_cpu_baseline)
+        torch.cuda.empty_cache()
+        anchor, _ = sharded_c3(args, 0, 1)
+        anchor["config"] = sharded_config()
+        anchor["note"] = ("N=1 point of the --gpus N strong-scaling line (K=2 parts, no "
+                          "exchange); --gpus N>1 prints this workload as its headline")
+        line["sharded_c3"] = anchor
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -443,6 +449,195 @@ def multilevel_cpu(xh, ah, cfg, plan, seconds=20.0):
                       f"extrapolated to the plan's passes"}
 
 
+SH_PASSES, SH_B = 80, 5
+
+
+def sharded_config():
+    """Workload keys of the multi-GPU line (identical for both arms)."""
+    return {"workload": "C3 finest level trained by the part-pair tournament sharded over the "
+                        "GPUs (SURVEY 8(e)): R-MAT scale 22, 126M sampled edges, ids densified, "
+                        "d=128, n_neg=3, B=5, balanced pools; one step = an 80-vertex-pass "
+                        "budget (rotations = 80 / (B K), K = 2 x GPUs parts); strong scaling",
+            "scale": C3_SCALE, "sampled_edges": C3_SAMPLES, "rmat_seed": C3_SEED,
+            "dim": C3_DIM, "negatives": NNEG, "batch": SH_B, "passes_per_step": SH_PASSES,
+            "lr": LR, "l2": "inputs larger than L2 (1.3 GiB matrix), no flush"}
+
+
+def sharded_cfg():
+    import paper_2008_12336_b200 as gb
+    return gb.TrainConfig(dim=C3_DIM, negative_samples=NNEG, seed=1, learning_rate=LR,
+                          balanced_pools=True, epoch_unit="vertex-pass")
+
+
+def sharded_c3(args, rank, world, print_line=True):
+    """The tournament step on C3 over `world` ranks (one per GPU; world 1 =
+    K=2 parts on one GPU, the strong-scaling anchor).  Each rank holds only
+    its two parts (PartStore); every off-diagonal round ends with an NCCL
+    P2P shift whose exposed time is measured with CUDA events."""
+    import torch
+    import paper_2008_12336_b200 as gb
+    from paper_2008_12336_b200 import tournament as tn
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = gb.rmat_graph(C3_SCALE, C3_SAMPLES, C3_SEED, densify_ids=True)
+    V = g.num_vertices
+    cfg = sharded_cfg()
+    local = [rank] if world > 1 else [0]
+    store = tn.PartStore(V, C3_DIM, world, local, dev)
+    store.init_random(cfg.seed)
+
+    def step(ev=None):
+        return tn.train_tournament_parts(g, store, cfg, SH_PASSES, batch_size=SH_B,
+                                         exchange_events=ev)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    events = []
+    upd = sent = 0
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            st = step(events)
+            upd += st["pos_updates"] + st["neg_updates"]
+            sent += st["exchange_bytes"]
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+    total_ms = t0.elapsed_time(t1)
+    exch_ms = sum(a.elapsed_time(b) for a, b in events)
+    if world > 1:
+        t = torch.tensor([total_ms, exch_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms, exch_ms = (float(x) for x in t.tolist())
+    value = upd / (total_ms / 1000.0)  # updates are summed over ranks by the driver
+    bpu = 8 * C3_DIM + (8 * C3_DIM) / (SH_B * (1 + NNEG))
+    peak, peak_src = measured_peak()
+    out = {"value": value, "unit": UNIT, "ms_per_step": total_ms / args.steps, "K": 2 * world,
+           "rotations_per_step": st["rotations"], "updates_per_step": upd // args.steps,
+           "roofline": {"bound": "hbm", "achieved": value * bpu / 1e9 / world, "peak": peak,
+                        "unit": "GB/s", "frac": value * bpu / 1e9 / world / peak,
+                        "traffic": None, "bytes_per_update": bpu, "peak_source": peak_src,
+                        "note": "per GPU, whole-step average including the exchanges"},
+           "exchange": {"bytes_per_step": sent // args.steps,
+                        "exposed_ms_per_step": exch_ms / args.steps,
+                        "exposed_share": exch_ms / total_ms if total_ms else 0.0,
+                        "nvlink_gbs_if_exposed": (sent / world / (exch_ms / 1000.0) / 1e9
+                                                  if exch_ms > 0 and sent else None)},
+           "part_bytes_per_gpu": store.device_bytes, "matrix_bytes": V * C3_DIM * 4,
+           "clocks": clk.summary()}
+    del store
+    return out, g
+
+
+def run_sharded(args):
+    """--gpus N > 1 (and --workload c3shard): the sharded C3 tournament step,
+    strong scaling (the same total updates per step at every N)."""
+    import torch
+    rank, world, local = dist_init()
+    import paper_2008_12336_b200 as gb
+    from paper_2008_12336_b200 import tournament as tn
+    res, g = sharded_c3(args, rank, world)
+    # e2e through the public API: train_tournament(g, pinned host matrix) --
+    # parts scattered from host memory, trained, gathered back every step
+    cfg = sharded_cfg()
+    M_host = torch.from_numpy(gb.init_embedding(g.num_vertices, C3_DIM, 1)).pin_memory()
+    tn.train_tournament(g, M_host, cfg, SH_PASSES, batch_size=SH_B)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e2e_steps = max(2, min(args.steps, 3))
+    te = time.perf_counter()
+    e_upd = 0
+    for _ in range(e2e_steps):
+        st = tn.train_tournament(g, M_host, cfg, SH_PASSES, batch_size=SH_B)
+        e_upd += st["pos_updates"] + st["neg_updates"]
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - te
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    K = 2 * world
+    part_bytes = -(-g.num_vertices // K) * C3_DIM * 4
+    line = {
+        "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 rows / f64 dot / f32 sigmoid",
+        "data": "synthetic R-MAT generated on device (seeded, Graph500 parameters)",
+        "config": sharded_config(),
+        "details": {"K": K, "vertices": g.num_vertices, "arcs": g.num_edges,
+                    "rotations_per_step": res["rotations_per_step"],
+                    "updates_per_step": res["updates_per_step"],
+                    "parallelism": f"tournament over {world} GPU(s), one process each, "
+                                   f"NCCL P2P part exchange",
+                    "part_bytes_per_gpu": res["part_bytes_per_gpu"],
+                    "matrix_bytes": res["matrix_bytes"]},
+        "roofline": res["roofline"], "exchange": res["exchange"],
+        "e2e": {"value": e_upd / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 2 * part_bytes,
+                "d2h_bytes_per_step": g.num_vertices * C3_DIM * 4,
+                "step": "train_tournament(g, M pinned host): 2 parts in, trained, all_gather "
+                        "back to every rank's host matrix", "steps": e2e_steps},
+        "gpu_launches": None, "clocks": res["clocks"],
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_sharded_reference(args):
+    """Reference arm of the multi-GPU line: the reference's partitioned pair
+    step (oracle restatement of _fill_pool_side + _train_pool_side,
+    bigtrain.py:164-238) on the same C3 graph and part count, all host
+    threads, a bounded sample of pairs."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+    threads = orc.max_threads()
+    x, a = orc.rmat_graph(C3_SCALE, C3_SAMPLES, C3_SEED, densify_ids=True)
+    V = len(x) - 1
+    K = 2 * world
+    bnd = (np.arange(K + 1, dtype=np.int64) * V) // K
+    M = orc.init_embedding(V, C3_DIM, 1)
+    upd, el, pairs = 0, 0.0, 0
+    for k in range(args.warmup + args.steps):
+        pa, pb = (k % K, (k + 1) % K)
+        la, ha, lb, hb = int(bnd[pa]), int(bnd[pa + 1]), int(bnd[pb]), int(bnd[pb + 1])
+        A = np.ascontiguousarray(M[la:ha])
+        Bm = np.ascontiguousarray(M[lb:hb])
+        t0 = time.perf_counter()
+        tj = orc.fill_pool_side(x, a, la, ha, lb, hb, SH_B, 7 + k, 0)
+        pos = orc.train_pool_side(A, Bm, tj, lb, hb - lb, NNEG, LR, 7 + k, 2, nthreads=threads)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            upd += pos * (1 + NNEG)
+            el += dt
+            pairs += 1
+    value = upd / el
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1000.0 / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 rows / f64 dot", "data": "synthetic R-MAT (CPU generator, bit-identical "
+                                              "to the GPU one)",
+        "config": sharded_config(),
+        "details": {"parallelism": f"{threads} host threads", "K": K},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{pairs} pair sides (fill_pool_side + train_pool_side, "
+                                   f"K={K} parts of the C3 graph), oracle/gosh_oracle.c"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
 def run_tournament(args):
     """Part-pair tournament (tournament.py) on the C2 graph: K = 2N parts,
     one step = one rotation (every pair once, K(K+1)/2 pair launches per
@@ -531,7 +726,10 @@ def main():
                     help="skip the C3 multilevel embed + AUCROC field")
     ap.add_argument("--c3-repeats", type=int, default=3)
     ap.add_argument("--c3-cpu-seconds", type=float, default=20.0)
-    ap.add_argument("--workload", choices=["c2", "tournament"], default="c2")
+    ap.add_argument("--workload", choices=["auto", "c2", "c3shard", "tournament"],
+                    default="auto",
+                    help="auto: c2 at N=1 (BASELINE configs[1]), c3shard at N>1 (configs[2] "
+                         "strong scaling)")
     ap.add_argument("--dim", type=int, default=0,
                     help="tournament workload: embedding dimension (default 128; C5 uses 256)")
     ap.add_argument("--virtual-ranks", type=int, default=1,
@@ -543,10 +741,21 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    workload = args.workload
+    if workload == "auto":
+        workload = "c3shard" if max(world, args.gpus) > 1 else "c2"
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator size in the log
     if args.impl == "reference":
-        run_reference(args)
-    elif args.workload == "tournament":
+        if workload == "c3shard":
+            run_sharded_reference(args)
+        else:
+            run_reference(args)
+    elif workload == "tournament":
         run_tournament(args)
+    elif workload == "c3shard":
+        run_sharded(args)
     else:
         run_ours(args)
 

@@ -144,79 +144,335 @@ class PairStep:
 PairFn = Callable[[torch.Tensor, torch.Tensor, PairStep], None]
 
 
-def device_pair_fn(g: Graph, cfg: TrainConfig, B: int,
-                   K: int = 1, status: torch.Tensor | None = None
-                   ) -> tuple[PairFn, torch.Tensor]:
+class DevicePair:
     """Pair step on the GPU: side 2 then side 3 (bigtrain.py:241-260) through
-    bigtrain.PairSides (compacted pools + list pair kernel by default);
-    returns (fn, status block).  Each fn owns its pool scratch, so fns made
-    with a shared status may run on different streams at once."""
-    _lib.require_cuda()
-    csr = g.device_csr()
-    flags = (_lib.GB_TRAIN_REUSE if cfg.reuse_updated_source else 0) | (
-        _lib.GB_TRAIN_EXACT if cfg.deterministic else _lib.GB_TRAIN_FAST_SIGMOID) | (
-        _lib.GB_TRAIN_ATOMIC if cfg.atomic_rows and not cfg.deterministic else 0)
-    if status is None:
-        status = _lib.new_status()
-    n_s = cfg.negative_samples
-    side_step = PairSides(csr, cfg, flags, B, status, K=K)
+    bigtrain.PairSides, split into prepare (the pools: they depend only on the
+    replicated CSR and the part ranges) and train (the pair kernels on the two
+    part buffers), with named pool buffer sets so the next round's pools are
+    drawn while the parts are still in flight between ranks."""
 
-    def fn(Ma: torch.Tensor, Mb: torch.Tensor, s: PairStep) -> None:
+    def __init__(self, g: Graph, cfg: TrainConfig, B: int, K: int = 1,
+                 status: torch.Tensor | None = None):
+        _lib.require_cuda()
+        flags = (_lib.GB_TRAIN_REUSE if cfg.reuse_updated_source else 0) | (
+            _lib.GB_TRAIN_EXACT if cfg.deterministic else _lib.GB_TRAIN_FAST_SIGMOID) | (
+            _lib.GB_TRAIN_ATOMIC if cfg.atomic_rows and not cfg.deterministic else 0)
+        self.status = status if status is not None else _lib.new_status()
+        self.sides = PairSides(g.device_csr(), cfg, flags, B, self.status, K=K)
+
+    def prepare(self, s: PairStep, tag: str = "0") -> None:
         if s.hi_a - s.lo_a <= 0 or s.hi_b - s.lo_b <= 0:
             return
-        side_step(Ma, Mb, s.lo_a, s.hi_a, s.lo_b, s.hi_b, s.seed, s.lr, 0, 2)
+        self.sides.prepare(s.lo_a, s.hi_a, s.lo_b, s.hi_b, s.seed, 0, tag + "a")
         if s.a != s.b:
-            side_step(Mb, Ma, s.lo_b, s.hi_b, s.lo_a, s.hi_a, s.seed, s.lr, 1, 3)
+            self.sides.prepare(s.lo_b, s.hi_b, s.lo_a, s.hi_a, s.seed, 1, tag + "b")
 
-    return fn, status
+    def train(self, Ma: torch.Tensor, Mb: torch.Tensor, s: PairStep, tag: str = "0") -> None:
+        if s.hi_a - s.lo_a <= 0 or s.hi_b - s.lo_b <= 0:
+            return
+        self.sides.train(Ma, Mb, s.lo_a, s.hi_a, s.lo_b, s.hi_b, s.seed, s.lr, 0, 2, tag + "a")
+        if s.a != s.b:
+            self.sides.train(Mb, Ma, s.lo_b, s.hi_b, s.lo_a, s.hi_a, s.seed, s.lr, 1, 3,
+                             tag + "b")
+
+    def __call__(self, Ma: torch.Tensor, Mb: torch.Tensor, s: PairStep) -> None:
+        self.prepare(s, "x")
+        self.train(Ma, Mb, s, "x")
+
+
+def device_pair_fn(g: Graph, cfg: TrainConfig, B: int, K: int = 1,
+                   status: torch.Tensor | None = None) -> tuple[DevicePair, torch.Tensor]:
+    """(pair step, status block); each step owns its pool scratch, so steps
+    made with a shared status may run on different streams at once."""
+    fn = DevicePair(g, cfg, B, K, status)
+    return fn, fn.status
 
 
 # ---------------------------------------------------------------------------
-# communication: real ranks (torch.distributed) or virtual ranks (one process)
+# part storage: a level's matrix as the parts this process holds
 # ---------------------------------------------------------------------------
-class _RankParts:
-    """The two part buffers of one rank plus their receive twins."""
+def init_embedding_rows(num_rows: int, dim: int, seed: int, lo: int, hi: int) -> np.ndarray:
+    """Rows [lo, hi) of init_embedding(num_rows, dim, seed) (trainer.py:87-93)
+    without drawing the others: numpy's uniform() consumes one PCG64 output
+    per value in row-major order, so the generator is advanced by lo*dim
+    outputs.  Bit-identical to the slice of the full draw."""
+    from .errors import ConfigError as _CE
+    if num_rows < 1 or dim < 1:
+        raise _CE("embedding dimensions must be positive")
+    bound = 0.5 / dim
+    bg = np.random.PCG64(seed)
+    bg.advance(lo * dim)
+    return np.random.Generator(bg).uniform(-bound, bound, size=(hi - lo, dim)).astype(np.float32)
 
-    def __init__(self, max_rows: int, dim: int, device, dtype=torch.float32):
-        self.cur = [torch.zeros((max_rows, dim), dtype=dtype, device=device) for _ in range(2)]
-        self.nxt = [torch.zeros((max_rows, dim), dtype=dtype, device=device) for _ in range(2)]
 
+class PartStore:
+    """One level's embedding matrix as the parts this process holds.
 
-def _exchange_dist(parts: _RankParts, rank: int, moves, group) -> int:
-    """Apply one shift on this rank with P2P send/recv; returns bytes sent.
-    A slot takes the part of a local move, else what it received, else it
-    keeps its part (position 0 never moves)."""
-    import torch.distributed as dist
-    ops, sent = [], 0
-    new = list(parts.cur)
-    received = set()
-    for sr, ss, dr, ds in moves:
-        if sr == rank and dr == rank:
-            new[ds] = parts.cur[ss]
-        elif sr == rank:
-            ops.append(dist.P2POp(dist.isend, parts.cur[ss], dr, group))
-            sent += parts.cur[ss].numel() * parts.cur[ss].element_size()
-        elif dr == rank:
-            ops.append(dist.P2POp(dist.irecv, parts.nxt[ds], sr, group))
-            received.add(ds)
-    if ops:
-        for w in dist.batch_isend_irecv(ops):
+    parts[r][slot] is the part id held in slot TOP/BOT by local rank r (one
+    rank per process under torch.distributed, every virtual rank otherwise)
+    and data[part] its rows, a (max_rows, d) buffer.  A process therefore
+    holds 2 parts per local rank (+ 2 receive twins with real ranks): 2|M|/G
+    per GPU, never the whole matrix (C5's 256 GiB matrix over
+    8 GPUs).
+
+    Host mode (`host=True`): the buffers are pinned host memory and a pair's
+    two parts are staged through device slots on a copy stream -- the
+    per-rank form of train_large's residency (bigtrain.py:263-340) for parts
+    that exceed the per-GPU budget.  The next local rank's parts load while
+    the current pair trains; trained parts flush back behind it."""
+
+    def __init__(self, V: int, d: int, G: int, local_ranks: list[int], device,
+                 host: bool = False):
+        self.V, self.d, self.G = V, d, G
+        self.K = 2 * G
+        self.plan = PartitionPlan(K=self.K,
+                                  boundaries=(np.arange(self.K + 1, dtype=np.int64) * V) // self.K)
+        self.local = list(local_ranks)
+        self.device = torch.device(device)
+        self.host = bool(host)
+        hold = holdings(initial_arrangement(self.K))
+        self.parts = {r: list(hold[r]) for r in self.local}
+        self.data: dict[int, torch.Tensor] = {}
+        for r in self.local:
+            for p in self.parts[r]:
+                self.data[p] = self._alloc()
+        self.spare: list[torch.Tensor] = []  # receive twins (real ranks)
+        self._stage = None
+
+    def _alloc(self) -> torch.Tensor:
+        if self.host:
+            return torch.zeros((self.plan.max_rows, self.d), dtype=torch.float32).pin_memory()
+        return torch.zeros((self.plan.max_rows, self.d), dtype=torch.float32, device=self.device)
+
+    @property
+    def device_bytes(self) -> int:
+        """HBM held for parts (the C5 budget figure): part buffers, receive
+        twins and staging slots."""
+        row = self.plan.max_rows * self.d * 4
+        n = 0 if self.host else len(self.data) + len(self.spare)
+        if self._stage is not None:
+            n += len(self._stage.slots)
+        return n * row
+
+    def rows(self, part: int) -> tuple[int, int]:
+        return self.plan.part_range(part)
+
+    def local_parts(self):
+        """(part, lo, hi, buffer rows) of every part this process holds."""
+        self.drain()
+        for r in self.local:
+            for p in self.parts[r]:
+                lo, hi = self.rows(p)
+                yield p, lo, hi, self.data[p][: hi - lo]
+
+    # -- filling ---------------------------------------------------------------
+    def load_full(self, Mt: torch.Tensor) -> None:
+        for p, lo, hi, buf in self.local_parts():
+            buf.copy_(Mt[lo:hi], non_blocking=True)
+
+    def init_random(self, seed: int) -> None:
+        """init_embedding(V, d, seed) restricted to the held rows."""
+        for p, lo, hi, buf in self.local_parts():
+            buf.copy_(torch.from_numpy(init_embedding_rows(self.V, self.d, seed, lo, hi)))
+
+    def expand_from(self, coarse: torch.Tensor, mapping) -> None:
+        """Row v of this level = row map[v] of the (replicated) coarser
+        matrix (trainer.py:243-249), gathered straight into the held parts:
+        the fine matrix is never materialised whole."""
+        cmap = mapping.device_map()
+        tmp = None
+        for p, lo, hi, buf in self.local_parts():
+            dst = buf
+            if self.host:
+                tmp = tmp if tmp is not None else torch.empty(
+                    (self.plan.max_rows, self.d), dtype=torch.float32, device=coarse.device)
+                dst = tmp[: hi - lo]
+            _lib.call("gb_expand", _lib.ptr(coarse), coarse.shape[0], self.d,
+                      cmap.data_ptr() + lo * cmap.element_size(), hi - lo, _lib.ptr(dst),
+                      _lib.stream())
+            if self.host:
+                buf.copy_(dst)
+
+    # -- output ------------------------------------------------------------------
+    def to_full(self, out: torch.Tensor | None = None, group=None, distributed: bool = False,
+                device=None) -> torch.Tensor:
+        """The whole matrix on every rank (all_gather of the parts; only at the
+        initial arrangement, i.e. between rotations)."""
+        dev = device if device is not None else self.device
+        self.drain()
+        if out is None:
+            out = torch.empty((self.V, self.d), dtype=torch.float32, device=dev)
+        hold = holdings(initial_arrangement(self.K))
+        if distributed:
+            import torch.distributed as dist
+            m = len(self.local)
+            mine = torch.stack([self.data[p] for r in self.local for p in self.parts[r]])
+            nccl = dist.get_backend(group) == "nccl"
+            mine = mine.to(self.device if nccl else "cpu")
+            bufs = [torch.empty_like(mine) for _ in range(self.G // m)]
+            dist.all_gather(bufs, mine, group=group)
+            for rr in range(self.G):
+                for slot, p in enumerate(hold[rr]):
+                    lo, hi = self.rows(p)
+                    out[lo:hi].copy_(bufs[rr // m][2 * (rr % m) + slot][: hi - lo])
+        else:
+            for p, lo, hi, buf in self.local_parts():
+                out[lo:hi].copy_(buf)
+        return out
+
+    # -- pair views ----------------------------------------------------------------
+    def begin_round(self, order: list[tuple[int, list[tuple[int, int]]]]) -> None:
+        """Host mode: stage the first local rank's parts of a round."""
+        if self.host:
+            if self._stage is None:
+                self._stage = _SlotStager(self)
+            self._stage.begin(order)
+
+    def pair_views(self, r: int, a: int, b: int) -> tuple[torch.Tensor, torch.Tensor]:
+        if self.host:
+            return self._stage.views(r, a, b)
+        lo_a, hi_a = self.rows(a)
+        lo_b, hi_b = self.rows(b)
+        Ma = self.data[a][: hi_a - lo_a]
+        return Ma, (Ma if a == b else self.data[b][: hi_b - lo_b])
+
+    def end_pair(self, r: int) -> None:
+        if self.host:
+            self._stage.done(r)
+
+    def end_round(self) -> None:
+        """Nothing to wait for: the next round's loads queue behind this
+        round's flushes on the copy stream."""
+
+    # -- exchange --------------------------------------------------------------
+    def shift(self, moves, arr: list[int], group=None, per_process: int = 0,
+              before_wait: Callable[[], None] | None = None) -> int:
+        """One circle shift (arrangement `arr` before it).  Moves between
+        ranks of this process relabel parts; with torch.distributed
+        (per_process = virtual ranks per process) a move to another process
+        is an NCCL (gloo on CPU) send/recv of one part, received into a spare
+        twin -- at most two sends and two receives per process, to its
+        neighbours.  `before_wait` runs after the transfers are posted (the
+        next round's pool draws overlap them).  Returns the bytes that left
+        a GPU (virtual ranks: that would have)."""
+        hold = holdings(arr)
+        local = set(self.local)
+        new = {r: list(self.parts[r]) for r in self.local}
+        row_bytes = self.plan.max_rows * self.d * 4
+        ops, sent, gone, arrived = [], 0, [], []
+        m = per_process
+        if m:
+            import torch.distributed as dist
+            self.drain()
+        for sr, ss, dr, ds in moves:
+            part = hold[sr][ss]
+            if sr in local and dr in local:
+                new[dr][ds] = part
+                if not m and sr != dr:
+                    sent += row_bytes
+            elif sr in local:
+                buf = self.data[part]
+                if self.host:  # sends go out of HBM
+                    buf = buf.to(self.device, non_blocking=True)
+                ops.append(dist.P2POp(dist.isend, buf, dr // m, group))
+                sent += buf.numel() * buf.element_size()
+                gone.append(part)
+            elif dr in local:
+                if not self.spare:
+                    self.spare.append(self._alloc())
+                buf = self.spare.pop()
+                rbuf = torch.empty_like(buf, device=self.device) if self.host else buf
+                ops.append(dist.P2POp(dist.irecv, rbuf, sr // m, group))
+                arrived.append((part, buf, rbuf))
+                new[dr][ds] = part
+        works = dist.batch_isend_irecv(ops) if ops else []
+        if before_wait is not None:
+            before_wait()
+        for w in works:
             w.wait()
-    for ds in received:
-        new[ds] = parts.nxt[ds]
-    used = {id(t) for t in new}
-    parts.nxt = [t for t in parts.cur + parts.nxt if id(t) not in used]
-    parts.cur = new
-    return sent
+        for part in gone:
+            self.spare.append(self.data.pop(part))
+        for part, buf, rbuf in arrived:
+            if rbuf is not buf:
+                buf.copy_(rbuf)
+            self.data[part] = buf
+        self.parts = new
+        return sent
+
+    def drain(self) -> None:
+        """Host mode: wait for outstanding flushes of trained parts."""
+        if self._stage is not None:
+            self._stage.drain()
 
 
-def _exchange_virtual(all_parts: list[_RankParts], moves) -> None:
-    """Apply one shift to every virtual rank by swapping buffer references."""
-    new = [list(p.cur) for p in all_parts]
-    for sr, ss, dr, ds in moves:
-        new[dr][ds] = all_parts[sr].cur[ss]
-    for r, p in enumerate(all_parts):
-        p.cur = new[r]
+class _SlotStager:
+    """Host-mode residency of a PartStore: two pairs of device slots, one copy
+    stream.  While local rank r trains in one slot pair, rank r+1's parts load
+    into the other; a pair's parts flush back to their pinned host buffers
+    behind its kernels (event-ordered), so PCIe copies overlap compute."""
+
+    def __init__(self, store: PartStore):
+        self.store = store
+        shape = (store.plan.max_rows, store.d)
+        self.slots = [torch.empty(shape, dtype=torch.float32, device=store.device)
+                      for _ in range(4)]
+        self.copy = torch.cuda.Stream(store.device)
+        self.order: list = []
+        self.loaded: dict[int, tuple[int, torch.cuda.Event, dict]] = {}
+        self.prefetched: set[int] = set()
+
+    def _load(self, idx: int) -> None:
+        r, pairs = self.order[idx]
+        base = 2 * (idx % 2)
+        parts = list(dict.fromkeys(p for pr in pairs for p in pr))
+        where = {}
+        compute = torch.cuda.current_stream(self.store.device)
+        fence = torch.cuda.Event()
+        fence.record(compute)  # the slot pair's previous kernels are queued before this
+        self.copy.wait_event(fence)
+        with torch.cuda.stream(self.copy):
+            for k, p in enumerate(parts):
+                lo, hi = self.store.rows(p)
+                self.slots[base + k][: hi - lo].copy_(self.store.data[p][: hi - lo],
+                                                      non_blocking=True)
+                where[p] = base + k
+        ev = torch.cuda.Event()
+        ev.record(self.copy)
+        self.loaded[r] = (idx, ev, where)
+
+    def begin(self, order) -> None:
+        self.order = list(order)
+        self.loaded = {}
+        self.prefetched = set()
+        if self.order:
+            self._load(0)
+
+    def views(self, r: int, a: int, b: int):
+        idx, ev, where = self.loaded[r]
+        torch.cuda.current_stream(self.store.device).wait_event(ev)
+        if idx + 1 < len(self.order) and idx + 1 not in self.prefetched:
+            self.prefetched.add(idx + 1)
+            self._load(idx + 1)  # prefetch the next rank behind this one's kernels
+        lo_a, hi_a = self.store.rows(a)
+        lo_b, hi_b = self.store.rows(b)
+        Ma = self.slots[where[a]][: hi_a - lo_a]
+        return Ma, (Ma if a == b else self.slots[where[b]][: hi_b - lo_b])
+
+    def done(self, r: int) -> None:
+        idx, _, where = self.loaded.pop(r)
+        compute = torch.cuda.current_stream(self.store.device)
+        trained = torch.cuda.Event()
+        trained.record(compute)
+        self.copy.wait_event(trained)
+        with torch.cuda.stream(self.copy):
+            for p, sl in where.items():
+                lo, hi = self.store.rows(p)
+                self.store.data[p][: hi - lo].copy_(self.slots[sl][: hi - lo], non_blocking=True)
+        # the slot pair is reused two ranks later: its next load waits on the
+        # compute stream (fence in _load) and runs after this flush (same stream)
+
+    def drain(self) -> None:
+        self.copy.synchronize()
 
 
 # ---------------------------------------------------------------------------
@@ -228,113 +484,145 @@ def _steps_for_round(rnd: list[tuple[int, int]], G: int, diagonal: bool):
     return [[rnd[r]] for r in range(G)]
 
 
-def train_tournament(g: Graph, M, cfg: TrainConfig, e_i: int, batch_size: int = 5,
-                     rng_stream: int = 0, group=None, num_ranks: int | None = None,
-                     pair_fn: PairFn | None = None, gather: bool = True) -> dict:
-    """Part-pair training of the level (g, M) for an e_i-epoch budget,
-    sharded over the ranks of `group` (torch.distributed; NCCL on GPUs), or
-    over `num_ranks` virtual ranks in this process when no process group is
-    initialised.  M is the full matrix, identical on every rank (CUDA
-    tensor, or numpy/CPU tensor staged to the rank's device); with gather
-    the trained matrix is written back into M on every rank.
-
-    pair_fn overrides the pair step (tests substitute a CPU checker to run
-    the schedule and exchange over gloo); the default is the device kernel.
-    Returns a stats dict in train_large's shape plus the exchange volume."""
-    cfg.validate()
-    if M.shape[0] != g.num_vertices:
-        raise ValueError("matrix rows must match vertex count")
+def _world(group, num_ranks, per_process: int = 1):
+    """(distributed, G ranks of the schedule, this process's ranks).  Under
+    torch.distributed each process runs `per_process` consecutive ranks of
+    the schedule (K = 2 * world * per_process parts); otherwise all
+    `num_ranks` are virtual ranks of this process."""
     import torch.distributed as dist
+    if per_process < 1:
+        raise ConfigError("per_process must be >= 1")
     distributed = dist.is_available() and dist.is_initialized()
     if distributed:
-        G, rank = dist.get_world_size(group), dist.get_rank(group)
-    else:
-        G, rank = (num_ranks or 1), -1
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        G = world * per_process
+        return True, G, list(range(rank * per_process, (rank + 1) * per_process))
+    G = num_ranks or 1
     if G < 1:
         raise ConfigError("num_ranks must be >= 1")
-    K, B, V, d = 2 * G, batch_size, M.shape[0], M.shape[1]
-    if V < K:
-        raise ConfigError(f"{V} rows cannot be split into {K} parts")
-    plan = PartitionPlan(K=K, boundaries=(np.arange(K + 1, dtype=np.int64) * V) // K)
+    return False, G, list(range(G))
+
+
+def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: int,
+                           batch_size: int = 5, rng_stream: int = 0, group=None,
+                           pair_fn: PairFn | None = None,
+                           exchange_events: list | None = None) -> dict:
+    """Part-pair training of the level (g, parts in `store`) for an e_i-epoch
+    budget.  Each rotation: a diagonal round, then K-1 off-diagonal rounds of
+    one pair per rank with a circle shift between rounds.  Between real ranks
+    the shift is posted as P2P transfers and the next round's pools are drawn
+    while they are in flight; virtual ranks relabel parts and run their pairs
+    on one stream each.  Returns train_large's stats plus exchange volume.
+    exchange_events, if given, collects (start, end) CUDA events around each
+    shift on the compute stream: the exposed (not overlapped) exchange time."""
+    cfg.validate()
+    import torch.distributed as dist
+    distributed = dist.is_available() and dist.is_initialized() and len(store.local) < store.G
+    per_process = len(store.local) if distributed else 0
+    G, K, B = store.G, store.K, batch_size
+    plan = store.plan
     rotations = tournament_rotations(g, cfg, e_i, K, B)
     rounds = tournament_rounds(K)
     index = pair_index(K)
     P = len(index)
     moves = shift_moves(K)
-    status = None
-    # virtual ranks on one GPU: each rank's pairs go to their own stream (the
-    # pairs of a round touch disjoint parts, as on G GPUs), joined once per
-    # round before the exchange.  Only small parts gain (C2, d=128: 32 MiB
-    # parts 3.14 -> 5.80 G upd/s; 64 MiB parts equal at d=128, -20% at
-    # d=256; 128 MiB parts -10%): GB_VIRTUAL_STREAMS auto (parts under
-    # 48 MiB) / 1 / 0
-    streams = None
     vs = os.environ.get("GB_VIRTUAL_STREAMS", "auto")
     if vs not in ("auto", "0", "1"):
         raise ConfigError(f"GB_VIRTUAL_STREAMS={vs!r}: expected auto, 0 or 1")
-    if pair_fn is None:
-        pair_fn, status = device_pair_fn(g, cfg, B, K)
-        device = torch.device("cuda", torch.cuda.current_device())
-        if not distributed and G > 1 and (
-                vs == "1" or (vs == "auto" and plan.max_rows * d * 4 < 48 << 20)):
-            streams = [torch.cuda.Stream(device) for _ in range(G)]
-            rank_fns = [pair_fn] + [device_pair_fn(g, cfg, B, K, status)[0]
-                                    for _ in range(G - 1)]
-    else:
-        device = M.device if isinstance(M, torch.Tensor) else torch.device("cpu")
-    Mt = M if isinstance(M, torch.Tensor) else torch.from_numpy(M)
-    if Mt.dtype != torch.float32:
-        raise TypeError("embedding matrix must be float32")
-
-    my_ranks = [rank] if distributed else list(range(G))
-    parts = {r: _RankParts(plan.max_rows, d, device) for r in my_ranks}
-    arr0 = initial_arrangement(K)
-    for r in my_ranks:
-        for slot, part in enumerate(holdings(arr0)[r]):
-            lo, hi = plan.part_range(part)
-            parts[r].cur[slot][: hi - lo].copy_(Mt[lo:hi], non_blocking=True)
+    status = None
+    streams = None
+    on_gpu = pair_fn is None
+    if on_gpu:
+        first, status = device_pair_fn(g, cfg, B, K)
+        fns = {r: first for r in store.local}
+        # virtual ranks: each rank's pairs on their own stream (the pairs of
+        # a round touch disjoint parts, as on G GPUs), joined once per round.
+        # Only small parts gain (C2, d=128: 32 MiB parts 3.14 -> 5.80 G upd/s;
+        # 64 MiB equal; 128 MiB -10%): GB_VIRTUAL_STREAMS auto (< 48 MiB) / 1 / 0
+        if not distributed and G > 1 and not store.host and (
+                vs == "1" or (vs == "auto" and plan.max_rows * store.d * 4 < 48 << 20)):
+            streams = {r: torch.cuda.Stream(store.device) for r in store.local}
+            fns = {r: device_pair_fn(g, cfg, B, K, status)[0] for r in store.local}
+    has_prepare = on_gpu
 
     sent_bytes, n_pairs = 0, 0
     t0 = time.perf_counter()
-    main = torch.cuda.current_stream(device) if streams else None
-    for rot in range(rotations):
-        lr = lr_at(cfg.learning_rate, rot, rotations)
-        arr = initial_arrangement(K)
-        for ri, rnd in enumerate(rounds):
-            diagonal = ri == 0
-            hold = holdings(arr)
-            per_rank = _steps_for_round(rnd, G, diagonal)
-            for r in my_ranks:
+    main = torch.cuda.current_stream(store.device) if store.device.type == "cuda" else None
+
+    def round_steps(rot, ri, arr):
+        diagonal = ri == 0
+        per_rank = _steps_for_round(rounds[ri], G, diagonal)
+        out = []
+        for r in store.local:
+            lst = []
+            for k, (a, b) in enumerate(per_rank[r]):
+                lo_a, hi_a = plan.part_range(a)
+                lo_b, hi_b = plan.part_range(b)
+                seed = _derived_seed(cfg.seed, rng_stream, rot * P + index[(a, b)])
+                lst.append((k, PairStep(a, b, lo_a, hi_a, lo_b, hi_b, seed,
+                                        lr_at(cfg.learning_rate, rot, rotations))))
+            out.append((r, lst))
+        return out
+
+    def prepare(steps, ri):
+        if not has_prepare:
+            return
+        for r, lst in steps:
+            ctx = torch.cuda.stream(streams[r]) if streams else _null()
+            with ctx:
                 if streams:
                     streams[r].wait_stream(main)
-                    pair_fn = rank_fns[r]
-                for a, b in per_rank[r]:
-                    slot_of = {hold[r][TOP]: TOP, hold[r][BOT]: BOT}
-                    Ma = parts[r].cur[slot_of[a]]
-                    Mb = Ma if a == b else parts[r].cur[slot_of[b]]
-                    lo_a, hi_a = plan.part_range(a)
-                    lo_b, hi_b = plan.part_range(b)
-                    seed = _derived_seed(cfg.seed, rng_stream, rot * P + index[(a, b)])
-                    step = PairStep(a, b, lo_a, hi_a, lo_b, hi_b, seed, lr)
+                for k, s in lst:
+                    fns[r].prepare(s, f"{ri % 2}.{k}.")
+
+    for rot in range(rotations):
+        arr = initial_arrangement(K)
+        steps = round_steps(rot, 0, arr)
+        prepare(steps, 0)
+        for ri in range(len(rounds)):
+            diagonal = ri == 0
+            store.begin_round([(r, [(s.a, s.b) for _, s in lst]) for r, lst in steps])
+            for r, lst in steps:
+                ctx = torch.cuda.stream(streams[r]) if streams else _null()
+                with ctx:
                     if streams:
-                        with torch.cuda.stream(streams[r]):
-                            pair_fn(Ma[: hi_a - lo_a], Mb[: hi_b - lo_b], step)
-                    else:
-                        pair_fn(Ma[: hi_a - lo_a], Mb[: hi_b - lo_b], step)
-                    n_pairs += 1
+                        streams[r].wait_stream(main)
+                    for k, s in lst:
+                        Ma, Mb = store.pair_views(r, s.a, s.b)
+                        if has_prepare:
+                            fns[r].train(Ma, Mb, s, f"{ri % 2}.{k}.")
+                        else:
+                            pair_fn(Ma, Mb, s)
+                        n_pairs += 1
+                    store.end_pair(r)
             if streams:
-                for st_r in streams:
+                for st_r in streams.values():
                     main.wait_stream(st_r)
+            store.end_round()
+            nxt = None
+            if ri + 1 < len(rounds):
+                arr_next = shift(arr) if not diagonal and K > 2 else arr
+                nxt = round_steps(rot, ri + 1, arr_next)
             if not diagonal and K > 2:
-                if distributed:
-                    sent_bytes += _exchange_dist(parts[rank], rank, moves, group)
-                else:
-                    _exchange_virtual([parts[r] for r in my_ranks], moves)
-                    sent_bytes += sum(plan.max_rows * d * 4 for sr, _, dr, _ in moves
-                                      if sr != dr)
+                after = (lambda: prepare(nxt, ri + 1)) if nxt else None
+                if exchange_events is not None and main is not None:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(main)
+                sent_bytes += store.shift(moves, arr, group, per_process=per_process,
+                                          before_wait=after if per_process else None)
+                if exchange_events is not None and main is not None:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(main)
+                    exchange_events.append((e0, e1))
+                if not per_process and after:
+                    after()
                 arr = shift(arr)
-    if device.type == "cuda":
-        torch.cuda.current_stream(device).synchronize()
+            elif nxt:
+                prepare(nxt, ri + 1)
+            steps = nxt
+    store.drain()
+    if store.device.type == "cuda":
+        torch.cuda.current_stream(store.device).synchronize()
     train_s = time.perf_counter() - t0
 
     pos_local = neg_local = 0
@@ -348,16 +636,9 @@ def train_tournament(g: Graph, M, cfg: TrainConfig, e_i: int, batch_size: int = 
     pos, neg = pos_local, neg_local
     if distributed:
         t = torch.tensor([pos_local, neg_local, n_pairs, sent_bytes], dtype=torch.int64,
-                         device=device if dist.get_backend(group) == "nccl" else "cpu")
+                         device=store.device if dist.get_backend(group) == "nccl" else "cpu")
         dist.all_reduce(t, group=group)
         pos, neg, n_pairs, sent_bytes = (int(x) for x in t.tolist())
-
-    if gather:
-        _gather(Mt, parts, plan, G, rank, distributed, group, device)
-        if not isinstance(M, torch.Tensor):
-            M[...] = Mt.numpy()
-        if not bool(torch.isfinite(Mt).all()):
-            raise FloatingPointError("non-finite embedding after tournament training")
     return {
         "rotations": rotations,
         "K": K,
@@ -368,28 +649,65 @@ def train_tournament(g: Graph, M, cfg: TrainConfig, e_i: int, batch_size: int = 
         "neg_updates": neg,
         "exchange_bytes": sent_bytes,
         "train_s": train_s,
+        "part_device_bytes": store.device_bytes,
     }
 
 
-def _gather(Mt: torch.Tensor, parts, plan: PartitionPlan, G: int, rank: int, distributed: bool,
-            group, device) -> None:
-    """Write every part back into the full matrix on every rank (the
-    arrangement is the initial one again after a whole rotation)."""
-    hold = holdings(initial_arrangement(plan.K))
-    if distributed:
-        import torch.distributed as dist
-        mine = torch.stack(parts[rank].cur)
-        if dist.get_backend(group) != "nccl" and mine.is_cuda:
-            mine = mine.cpu()
-        bufs = [torch.empty_like(mine) for _ in range(G)]
-        dist.all_gather(bufs, mine, group=group)
-        src = {r: bufs[r] for r in range(G)}
+class _null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+def train_tournament(g: Graph, M, cfg: TrainConfig, e_i: int, batch_size: int = 5,
+                     rng_stream: int = 0, group=None, num_ranks: int | None = None,
+                     pair_fn: PairFn | None = None, gather: bool = True,
+                     host_parts: bool = False, per_process: int = 1) -> dict:
+    """Part-pair training of the level (g, M) for an e_i-epoch budget,
+    sharded over the ranks of `group` (torch.distributed; NCCL on GPUs), or
+    over `num_ranks` virtual ranks in this process when no process group is
+    initialised.  M is the full matrix, identical on every rank (CUDA
+    tensor, or numpy/CPU tensor); each rank copies only its two parts in,
+    trains them (PartStore), and with gather the trained matrix is written
+    back into M on every rank.  host_parts keeps the parts in pinned host
+    memory, staged through device slots (budget mode); per_process runs that
+    many consecutive schedule ranks in each process (K = 2 * world *
+    per_process).
+
+    pair_fn overrides the pair step (tests substitute a CPU checker to run
+    the schedule and exchange over gloo); the default is the device kernel.
+    Returns a stats dict in train_large's shape plus the exchange volume."""
+    cfg.validate()
+    if M.shape[0] != g.num_vertices:
+        raise ValueError("matrix rows must match vertex count")
+    distributed, G, local = _world(group, num_ranks, per_process)
+    K, V, d = 2 * G, M.shape[0], M.shape[1]
+    if V < K:
+        raise ConfigError(f"{V} rows cannot be split into {K} parts")
+    vs = os.environ.get("GB_VIRTUAL_STREAMS", "auto")
+    if vs not in ("auto", "0", "1"):
+        raise ConfigError(f"GB_VIRTUAL_STREAMS={vs!r}: expected auto, 0 or 1")
+    if pair_fn is None:
+        _lib.require_cuda()
+        device = torch.device("cuda", torch.cuda.current_device())
     else:
-        src = {r: parts[r].cur for r in range(G)}
-    for r in range(G):
-        for slot, part in enumerate(hold[r]):
-            lo, hi = plan.part_range(part)
-            Mt[lo:hi].copy_(src[r][slot][: hi - lo])
+        device = M.device if isinstance(M, torch.Tensor) else torch.device("cpu")
+    Mt = M if isinstance(M, torch.Tensor) else torch.from_numpy(M)
+    if Mt.dtype != torch.float32:
+        raise TypeError("embedding matrix must be float32")
+    store = PartStore(V, d, G, local, device, host=host_parts)
+    store.load_full(Mt)
+    st = train_tournament_parts(g, store, cfg, e_i, batch_size=batch_size,
+                                rng_stream=rng_stream, group=group, pair_fn=pair_fn)
+    if gather:
+        store.to_full(out=Mt, group=group, distributed=distributed, device=Mt.device)
+        if not isinstance(M, torch.Tensor):
+            M[...] = Mt.numpy()
+        if not bool(torch.isfinite(Mt).all()):
+            raise FloatingPointError("non-finite embedding after tournament training")
+    return st
 
 
 def sequential_order(K: int, rotations: int):
@@ -407,13 +725,24 @@ def sequential_order(K: int, rotations: int):
 def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
                              shard_levels: int = 1, batch_size: int = 5, group=None,
                              num_ranks: int | None = None, hierarchy=None,
-                             return_device: bool = False, balanced_pools: bool = True):
+                             return_device: bool = False, balanced_pools: bool = True,
+                             return_parts: bool = False, host_parts: bool = False,
+                             per_process: int = 1):
     """train_multilevel (trainer.py:252-288) with the finest `shard_levels`
-    levels trained by the tournament across ranks.  Every rank coarsens
-    (the device collapse is deterministic, so the hierarchies are identical
-    with no communication); the coarse levels train on rank 0 and the matrix
-    is broadcast before the first sharded level.  Returns
-    (matrix, per-level stats).
+    levels trained by the tournament across ranks.
+
+    Every rank coarsens (the device collapse is deterministic, so the
+    hierarchies are identical with no communication).  Levels above the
+    sharded ones are small: they train on rank 0 and the matrix is broadcast
+    once.  The first sharded level is expanded from that matrix straight into
+    each rank's two parts; a further sharded level all-gathers the coarser
+    level's parts (the coarse matrix is ~5x smaller) and expands into its
+    own parts.  So no rank ever holds a whole sharded level: per GPU the
+    finest level costs 2|M|/G plus two receive twins (C5: 64 GiB of parts,
+    or pinned host parts with `host_parts`).
+
+    Returns (matrix, per-level stats); with return_parts the finest level
+    stays sharded and the first element is its PartStore (rows per rank).
 
     balanced_pools (default; Hogwild runs only): the sharded levels draw
     balanced pools (TrainConfig.balanced_pools), which keeps this path's
@@ -426,7 +755,7 @@ def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
     cfg.validate()
     if balanced_pools and not cfg.deterministic and not cfg.balanced_pools:
         cfg = dataclasses.replace(cfg, balanced_pools=True)
-    distributed = dist.is_available() and dist.is_initialized()
+    distributed, G, local = _world(group, num_ranks, per_process)
     rank = dist.get_rank(group) if distributed else 0
     if hierarchy is None:
         hierarchy = coarsen_all(g0, threshold=threshold)
@@ -435,22 +764,30 @@ def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
     plan = (np.zeros(depth, dtype=np.int64) if cfg.total_epochs == 0
             else epoch_plan(cfg.total_epochs, cfg.smoothing_ratio, depth).per_level)
     _lib.require_cuda()
-    M = torch.from_numpy(init_embedding(hierarchy.graphs[-1].num_vertices, cfg.dim,
-                                        cfg.seed)).cuda()
+    device = torch.device("cuda", torch.cuda.current_device())
+
+    def sharded(i):
+        return i < shard_levels and hierarchy.graphs[i].num_vertices >= 2 * G
+
     stats = []
+    M = None       # replicated full matrix of the current (unsharded) level
+    store = None   # parts of the current sharded level
+    top = depth - 1
+    if sharded(top):
+        store = PartStore(hierarchy.graphs[top].num_vertices, cfg.dim, G, local, device,
+                          host=host_parts)
+        store.init_random(cfg.seed)
+    else:
+        M = torch.from_numpy(init_embedding(hierarchy.graphs[top].num_vertices, cfg.dim,
+                                            cfg.seed)).cuda()
     broadcast_done = False
     for i in range(depth - 1, -1, -1):
         g_i = hierarchy.graphs[i]
         e_i = int(plan[i])
-        sharded = i < shard_levels and g_i.num_vertices >= 2 * (
-            dist.get_world_size(group) if distributed else (num_ranks or 1))
         t0 = time.perf_counter()
-        if sharded and e_i > 0:
-            if distributed and not broadcast_done:
-                dist.broadcast(M, 0, group=group)
-                broadcast_done = True
-            st = train_tournament(g_i, M, cfg, e_i, batch_size=batch_size, rng_stream=i,
-                                  group=group, num_ranks=num_ranks)
+        if store is not None:
+            st = train_tournament_parts(g_i, store, cfg, e_i, batch_size=batch_size,
+                                        rng_stream=i, group=group) if e_i > 0 else {}
             entry = {"level": i, "sharded": True, **st}
         else:
             entry = {"level": i, "sharded": False, "passes": 0, "updates": 0}
@@ -460,8 +797,31 @@ def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
         torch.cuda.synchronize()
         entry["s"] = time.perf_counter() - t0
         stats.append(entry)
-        if i > 0:
-            M = expand_embedding(M, hierarchy.mappings[i - 1])
-    if distributed and not broadcast_done:
+        if i == 0:
+            break
+        mapping = hierarchy.mappings[i - 1]
+        if sharded(i - 1):
+            if store is None:  # first sharded level: from the replicated coarse matrix
+                if distributed and not broadcast_done:
+                    dist.broadcast(M, 0, group=group)
+                    broadcast_done = True
+                coarse = M
+            else:              # coarser level sharded too: gather it (it is ~5x smaller)
+                coarse = store.to_full(group=group, distributed=distributed)
+            store = PartStore(hierarchy.graphs[i - 1].num_vertices, cfg.dim, G, local, device,
+                              host=host_parts)
+            store.expand_from(coarse, mapping)
+            del coarse
+            M = None
+        else:
+            if store is not None:  # (not reached with the default finest-first sharding)
+                M = store.to_full(group=group, distributed=distributed)
+                store = None
+            M = expand_embedding(M, mapping)
+    if store is not None:
+        if return_parts:
+            return store, stats
+        M = store.to_full(group=group, distributed=distributed)
+    elif distributed and not broadcast_done:
         dist.broadcast(M, 0, group=group)
     return (M if return_device else M.cpu().numpy()), stats

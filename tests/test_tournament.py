@@ -121,7 +121,7 @@ def test_virtual_ranks_equal_sequential_replay(orc, G):
     assert not np.array_equal(ref, M0)
 
 
-def _gloo_worker(rank, world, port, out_path):
+def _gloo_worker(rank, world, port, out_path, per_process=1):
     import torch.distributed as dist
     from oracle import oracle as orc
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -131,7 +131,8 @@ def _gloo_worker(rank, world, port, out_path):
         g, x, a = _graph(orc)
         cfg = gb.TrainConfig(dim=16, negative_samples=3, seed=3, deterministic=True)
         M = torch.from_numpy(orc.init_embedding(g.num_vertices, 16, 1))
-        st = tn.train_tournament(g, M, cfg, 30, pair_fn=_oracle_pair_fn(orc, x, a, 5, 3))
+        st = tn.train_tournament(g, M, cfg, 30, pair_fn=_oracle_pair_fn(orc, x, a, 5, 3),
+                                 per_process=per_process)
         np.save(f"{out_path}.{rank}.npy", M.numpy())
         np.save(f"{out_path}.{rank}.stats.npy",
                 np.array([st["pairs"], st["exchange_bytes"], st["ranks"]]))
@@ -139,8 +140,11 @@ def _gloo_worker(rank, world, port, out_path):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_gloo_tournament_equals_sequential_replay(orc, world):
+@pytest.mark.parametrize("world,per_process", [(2, 1), (3, 1), (4, 1), (2, 2)])
+def test_gloo_tournament_equals_sequential_replay(orc, world, per_process):
+    """K = 2 * world * per_process parts over `world` gloo processes: the
+    schedule, the P2P shift (per_process=2 mixes in-process relabels with
+    cross-process sends) and the all_gather equal the sequential replay."""
     import socket
 
     import torch.multiprocessing as mp
@@ -149,20 +153,28 @@ def test_gloo_tournament_equals_sequential_replay(orc, world):
         port = s.getsockname()[1]
     with tempfile.TemporaryDirectory() as td:
         out = os.path.join(td, "m")
-        mp.spawn(_gloo_worker, args=(world, port, out), nprocs=world, join=True)
+        mp.spawn(_gloo_worker, args=(world, port, out, per_process), nprocs=world, join=True)
         g, x, a = _graph(orc)
         cfg = gb.TrainConfig(dim=16, negative_samples=3, seed=3, deterministic=True)
         ref = orc.init_embedding(g.num_vertices, 16, 1)
-        rot = _sequential_replay(orc, g, x, a, ref, cfg, 30, world)
-        K = 2 * world
+        G = world * per_process
+        rot = _sequential_replay(orc, g, x, a, ref, cfg, 30, G)
+        K = 2 * G
         for r in range(world):
             M = np.load(f"{out}.{r}.npy")
             assert np.array_equal(M, ref), f"rank {r}"
             pairs, sent, ranks = np.load(f"{out}.{r}.stats.npy").tolist()
-            assert ranks == world and pairs == rot * K * (K + 1) // 2
-            # every rank sends <= 2 parts per shift; K-1 shifts per rotation
+            assert ranks == G and pairs == rot * K * (K + 1) // 2
+            # every process sends <= 2 parts per shift; K-1 shifts per rotation
             max_rows = -(-g.num_vertices // K)
             assert 0 < sent <= rot * (K - 1) * world * 2 * max_rows * 16 * 4
+
+
+def test_init_embedding_rows_equals_slice_of_full_draw():
+    for V, d, seed in [(1000, 16, 1), (77, 33, 9), (5, 128, 2)]:
+        full = gb.init_embedding(V, d, seed)
+        for lo, hi in [(0, V), (0, 1), (V // 3, V // 2), (V - 1, V)]:
+            assert np.array_equal(tn.init_embedding_rows(V, d, seed, lo, hi), full[lo:hi])
 
 
 # -- GPU: device pair kernel under the tournament ----------------------------------
@@ -177,6 +189,43 @@ def test_device_tournament_deterministic_bit_exact(cuda, orc, G):
     M = torch.from_numpy(M0.copy()).cuda()
     tn.train_tournament(g, M, cfg, 20, num_ranks=G)
     assert np.array_equal(M.cpu().numpy(), ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G", [2, 3])
+def test_host_staged_parts_deterministic_bit_exact(cuda, orc, G):
+    """Parts in pinned host memory staged through four device slots (the
+    budget mode for levels whose parts exceed HBM) equal the sequential
+    replay bit for bit, and only the slots occupy HBM."""
+    g, x, a = _graph(orc, scale=10, samples=6000)
+    cfg = gb.TrainConfig(dim=32, negative_samples=3, seed=4, deterministic=True)
+    M0 = orc.init_embedding(g.num_vertices, 32, 2)
+    ref = M0.copy()
+    _sequential_replay(orc, g, x, a, ref, cfg, 20, G)
+    M = M0.copy()
+    st = tn.train_tournament(g, M, cfg, 20, num_ranks=G, host_parts=True)
+    assert np.array_equal(M, ref)
+    max_rows = -(-g.num_vertices // (2 * G))
+    assert st["part_device_bytes"] == 4 * max_rows * 32 * 4
+
+
+@pytest.mark.gpu
+def test_sharded_multilevel_holds_only_parts(cuda, orc):
+    """train_multilevel_sharded expands the coarse matrix straight into each
+    rank's parts: with return_parts the finest level never exists whole on
+    the device; gathering the parts gives the full-matrix path's result
+    (deterministic kernels, virtual ranks)."""
+    g, x, a = _graph(orc, scale=11, samples=20000)
+    cfg = gb.TrainConfig(dim=32, total_epochs=20, negative_samples=3, seed=4,
+                         deterministic=True)
+    ref, _ = gb.train_multilevel_sharded(g, cfg, num_ranks=4)
+    store, stats = gb.train_multilevel_sharded(g, cfg, num_ranks=4, return_parts=True)
+    assert isinstance(store, tn.PartStore) and stats[-1]["sharded"]
+    assert np.array_equal(store.to_full().cpu().numpy(), ref)
+    store_h, _ = gb.train_multilevel_sharded(g, cfg, num_ranks=4, return_parts=True,
+                                             host_parts=True)
+    assert np.array_equal(store_h.to_full().cpu().numpy(), ref)
+    assert store_h.device_bytes < g.num_vertices * 32 * 4
 
 
 @pytest.mark.gpu
@@ -238,6 +287,50 @@ def _nccl_worker(rank, world, port, out_path):
         np.save(f"{out_path}.{rank}.npy", M)
     finally:
         dist.destroy_process_group()
+
+
+def _nccl_tournament_worker(rank, world, port, out_path):
+    import torch.distributed as dist
+    from oracle import oracle as orc
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        g, x, a = _graph(orc, scale=10, samples=6000)
+        cfg = gb.TrainConfig(dim=32, negative_samples=3, seed=4, deterministic=True)
+        M = torch.from_numpy(orc.init_embedding(g.num_vertices, 32, 2)).cuda()
+        st = tn.train_tournament(g, M, cfg, 20)
+        np.save(f"{out_path}.{rank}.npy", M.cpu().numpy())
+        np.save(f"{out_path}.{rank}.sent.npy", np.array([st["exchange_bytes"]]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_two_ranks_exchange_equals_sequential_replay(cuda, orc):
+    """Two real ranks (one GPU each): K = 4 parts, so every off-diagonal round
+    ends with an NCCL P2P part exchange over NVLink (_the_ multi-GPU data
+    path); the result equals the sequential replay bit for bit."""
+    import socket
+
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs (gloo world 2-4 covers the exchange on CPU)")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "m")
+        mp.spawn(_nccl_tournament_worker, args=(2, port, out), nprocs=2, join=True)
+        g, x, a = _graph(orc, scale=10, samples=6000)
+        cfg = gb.TrainConfig(dim=32, negative_samples=3, seed=4, deterministic=True)
+        ref = orc.init_embedding(g.num_vertices, 32, 2)
+        _sequential_replay(orc, g, x, a, ref, cfg, 20, 2)
+        for r in range(2):
+            assert np.array_equal(np.load(f"{out}.{r}.npy"), ref)
+            assert int(np.load(f"{out}.{r}.sent.npy")[0]) > 0
 
 
 @pytest.mark.gpu
