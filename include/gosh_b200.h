@@ -76,6 +76,44 @@ int gb_csr_build(int64_t num_vertices, const int64_t *src, const int64_t *dst,
                  int64_t *num_edges_out, void *workspace, size_t ws_bytes,
                  void *stream_handle);
 
+/* Row-block ("chunked") CSR construction, for graphs whose one-shot key
+ * buffers (24 B per arc) exceed the device (C5: ~8B arcs).  Same result as
+ * gb_csr_build / gb_coarse_csr, bit for bit, block by block:
+ *   gb_arc_histogram     hist[s] += arcs with source s (int64[V], caller
+ *                        zeroes; self-loops dropped / reversed arcs added
+ *                        per flags) -- the host picks row blocks from it;
+ *   gb_arc_keys_range    append key (s - r0) * V + d of every arc with
+ *                        r0 <= s < r1 at keys[*cursor..] (device cursor);
+ *   gb_mapped_histogram / gb_mapped_keys_range
+ *                        the same for the coarse arcs (cmap[v], cmap[u]) of
+ *                        a CSR with intra-cluster arcs dropped
+ *                        (coarsen.py:200-253), by coarse row block;
+ *   gb_keys_to_rows      sort + deduplicate a block's keys and write its
+ *                        rows: xadj_rows[0..rows) offset by `base` and
+ *                        adj_out[0..unique); synchronizes, *num_unique_out
+ *                        is a host pointer.
+ * gb_rmat_edges_range generates R-MAT samples first .. first+count-1 (each a
+ * pure function of its index), so sample batches never coexist. */
+int gb_arc_histogram(const int64_t *src, const int64_t *dst, int64_t num_arcs,
+                     unsigned flags, int64_t *hist, void *stream_handle);
+int gb_arc_keys_range(const int64_t *src, const int64_t *dst, int64_t num_arcs,
+                      unsigned flags, int64_t num_vertices, int64_t r0, int64_t r1,
+                      uint64_t *keys, int64_t *cursor, void *stream_handle);
+int gb_mapped_histogram(const int64_t *xadj, const int32_t *adj, int64_t num_vertices,
+                        const int32_t *cmap, int64_t *hist, void *stream_handle);
+int gb_mapped_keys_range(const int64_t *xadj, const int32_t *adj, int64_t num_vertices,
+                         const int32_t *cmap, int64_t num_clusters, int64_t c0,
+                         int64_t c1, uint64_t *keys, int64_t *cursor, void *stream_handle);
+int gb_keys_to_rows_workspace(int64_t num_keys, int64_t rows, int64_t num_cols,
+                              size_t *bytes);
+int gb_keys_to_rows(uint64_t *keys, int64_t num_keys, int64_t rows, int64_t num_cols,
+                    int64_t base, int64_t *xadj_rows, int32_t *adj_out,
+                    int64_t *num_unique_out, void *workspace, size_t ws_bytes,
+                    void *stream_handle);
+int gb_rmat_edges_range(int scale, int64_t first, int64_t count, double t_a, double t_ab,
+                        double t_abc, uint64_t seed, const int64_t *perm, int64_t *src,
+                        int64_t *dst, void *stream_handle);
+
 /* Drop isolated vertices and re-densify ids in ascending order -- the
  * load_edge_list convention (graph.py:160-164) applied to a CSR.  new_id
  * receives the old->new map (-1 for dropped ids); kept receives new->old.

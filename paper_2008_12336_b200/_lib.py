@@ -54,6 +54,13 @@ SIGNATURES = {
     "gb_coarse_csr": (_int, [_i64, _i64, _p, _p, _p, _i64, _p, _p, _pi64, _p, _sz, _p]),
     "gb_expand": (_int, [_p, _i64, _int, _p, _i64, _p, _p]),
     "gb_checksum": (_int, [_p, _i64, _int, _p, _p]),
+    "gb_arc_histogram": (_int, [_p, _p, _i64, C.c_uint, _p, _p]),
+    "gb_arc_keys_range": (_int, [_p, _p, _i64, C.c_uint, _i64, _i64, _i64, _p, _p, _p]),
+    "gb_mapped_histogram": (_int, [_p, _p, _i64, _p, _p, _p]),
+    "gb_mapped_keys_range": (_int, [_p, _p, _i64, _p, _i64, _i64, _i64, _p, _p, _p]),
+    "gb_keys_to_rows_workspace": (_int, [_i64, _i64, _i64, _psz]),
+    "gb_keys_to_rows": (_int, [_p, _i64, _i64, _i64, _i64, _p, _p, _pi64, _p, _sz, _p]),
+    "gb_rmat_edges_range": (_int, [_int, _i64, _i64, _dbl, _dbl, _dbl, _u64, _p, _p, _p, _p]),
     "gb_train_passes": (_int, [_i64, _p, _p, _p, _i64, _p, _int, _int, _u64, _u64, _i64, _i64,
                                _i64, _p, C.c_uint, _i64, _p, _p]),
     "gb_active_sources_workspace": (_int, [_i64, _psz]),

@@ -156,12 +156,28 @@ def collapse_map_parallel(g: Graph, order, num_workers: int) -> Mapping:
     return collapse_map(g, order)
 
 
-def build_coarse_graph(g: Graph, m: Mapping, num_workers: int = 1) -> Graph:
+def build_coarse_graph(g: Graph, m: Mapping, num_workers: int = 1,
+                       max_block_keys: int | None = None) -> Graph:
     """Contract g along m: clusters become vertices, parallel arcs merged,
-    self-loops dropped, rows sorted (coarsen.py:256-281)."""
+    self-loops dropped, rows sorted (coarsen.py:256-281).  max_block_keys
+    builds the coarse rows block by block (gb_mapped_keys_range +
+    gb_keys_to_rows) so the key scratch is bounded instead of 24 B per arc;
+    the result is identical."""
     xadj, adj = g.device_csr()
     cmap = m.device_map()
     V, E, nc = g.num_vertices, g.num_edges, m.num_clusters
+    if max_block_keys is not None:
+        from .graph import csr_from_blocks
+        st = _lib.stream()
+        hist = torch.zeros(nc, dtype=torch.int64, device="cuda")
+        _lib.call("gb_mapped_histogram", _lib.ptr(xadj), _lib.ptr(adj), V, _lib.ptr(cmap),
+                  _lib.ptr(hist), st)
+
+        def fill(c0, c1, keys, cursor):
+            _lib.call("gb_mapped_keys_range", _lib.ptr(xadj), _lib.ptr(adj), V, _lib.ptr(cmap),
+                      nc, c0, c1, _lib.ptr(keys), _lib.ptr(cursor), st)
+
+        return csr_from_blocks(nc, nc, hist, fill, max_block_keys, directed=g.directed)
     ws, wsb = _lib.workspace("gb_coarse_csr_workspace", V, E, nc)
     x2 = torch.empty(nc + 1, dtype=torch.int64, device="cuda")
     a2 = torch.empty(max(E, 1), dtype=torch.int32, device="cuda")
@@ -174,10 +190,12 @@ def build_coarse_graph(g: Graph, m: Mapping, num_workers: int = 1) -> Graph:
     return Graph(nc, E2, directed=g.directed, xadj_dev=x2, adj_dev=a2)
 
 
-def coarsen_all(g: Graph, threshold: int = 100, num_workers: int = 1) -> Hierarchy:
+def coarsen_all(g: Graph, threshold: int = 100, num_workers: int = 1,
+                max_block_keys: int | None = None) -> Hierarchy:
     """order -> collapse -> contract until |V| <= threshold; a level keeping
     more than 99% of the vertices is discarded and flags a stall
-    (coarsen.py:284-311).  num_workers is accepted for API parity."""
+    (coarsen.py:284-311).  num_workers is accepted for API parity;
+    max_block_keys bounds the coarse-CSR key scratch (build_coarse_graph)."""
     if threshold < 1:
         raise ConfigError("threshold must be >= 1")
     if num_workers < 1:
@@ -192,7 +210,7 @@ def coarsen_all(g: Graph, threshold: int = 100, num_workers: int = 1) -> Hierarc
         if m.num_clusters > STALL_RATIO * cur.num_vertices:
             stalled = True
             break
-        nxt = build_coarse_graph(cur, m)
+        nxt = build_coarse_graph(cur, m, max_block_keys=max_block_keys)
         torch.cuda.current_stream().synchronize()
         level_ms.append((time.perf_counter() - t0) * 1000.0)
         graphs.append(nxt)

@@ -199,6 +199,32 @@ __global__ void perm_keys(int64_t n, uint64_t pkey, uint64_t *__restrict__ keys,
   }
 }
 
+// samples first .. first + n - 1 (a sample is a pure function of its index)
+__global__ void rmat_range_kernel(int scale, int64_t first, int64_t n, double ta, double tab,
+                                  double tabc, uint64_t seed, const int64_t *__restrict__ perm,
+                                  int64_t *__restrict__ src, int64_t *__restrict__ dst) {
+  GRID_STRIDE(i, n) {
+    const int64_t e = first + i;
+    const uint64_t key = stream_key(seed, kRmatStream, (uint64_t)e, 0);
+    int64_t u = 0, v = 0;
+    for (int l = 0; l < scale; ++l) {
+      const double r = draw_unit(key, (uint64_t)l);
+      const int64_t bit = int64_t(1) << (scale - 1 - l);
+      if (r < ta) {
+      } else if (r < tab) {
+        v |= bit;
+      } else if (r < tabc) {
+        u |= bit;
+      } else {
+        u |= bit;
+        v |= bit;
+      }
+    }
+    src[i] = perm ? perm[u] : u;
+    dst[i] = perm ? perm[v] : v;
+  }
+}
+
 __global__ void rmat_kernel(int scale, int64_t n, double ta, double tab, double tabc,
                             uint64_t seed, const int64_t *__restrict__ perm,
                             int64_t *__restrict__ src, int64_t *__restrict__ dst) {
@@ -834,6 +860,255 @@ GB_API int gb_checksum(const void *data, int64_t n, int elem_bytes, uint64_t *ou
     checksum_kernel<<<grid, 256, 0, st>>>(static_cast<const int32_t *>(data), n, o);
   else
     checksum_kernel<<<grid, 256, 0, st>>>(static_cast<const int64_t *>(data), n, o);
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Row-block (chunked) CSR construction.  The one-shot builds above hold the
+// keys of every arc three times over (keys, sorted copy, unique copy: 24 B
+// per arc, ~190 GB for C5's 8B arcs); here only one block of source rows
+// [r0, r1) is keyed, sorted and emitted at a time, so the scratch scales
+// with the block.  The host picks blocks from a per-source arc histogram
+// (an upper bound: duplicates are counted until the block's unique pass)
+// and streams the arcs through in batches (device arc arrays, R-MAT sample
+// batches, or a CSR mapped through a cluster map for the coarse graph).
+// Blocks emit rows in order, so the concatenated output is the one-shot
+// build's CSR bit for bit.
+// ---------------------------------------------------------------------------
+__global__ void arc_hist_kernel(const int64_t *__restrict__ src, const int64_t *__restrict__ dst,
+                                int64_t n, bool drop_self, bool sym,
+                                unsigned long long *__restrict__ hist) {
+  GRID_STRIDE(i, n) {
+    const int64_t s = src[i], d = dst[i];
+    if (drop_self && s == d) continue;
+    atomicAdd(hist + s, 1ull);
+    if (sym) atomicAdd(hist + d, 1ull);
+  }
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// keys (s - r0) * V + d of the arcs whose source lies in [r0, r1), appended
+// at a warp-aggregated cursor (order inside the block is irrelevant: sorted next)
+__global__ void arc_keys_range_kernel(const int64_t *__restrict__ src,
+                                      const int64_t *__restrict__ dst, int64_t n, bool drop_self,
+                                      bool sym, int64_t r0, int64_t r1, uint64_t V,
+                                      uint64_t *__restrict__ keys,
+                                      unsigned long long *__restrict__ cursor) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < n;
+       i0 += stride) {
+    const int64_t i = i0 + lane;
+    bool e1 = false, e2 = false;
+    uint64_t k1 = 0, k2 = 0;
+    if (i < n) {
+      const int64_t s = src[i], d = dst[i];
+      if (!(drop_self && s == d)) {
+        if (s >= r0 && s < r1) {
+          e1 = true;
+          k1 = (uint64_t)(s - r0) * V + (uint64_t)d;
+        }
+        if (sym && d >= r0 && d < r1) {
+          e2 = true;
+          k2 = (uint64_t)(d - r0) * V + (uint64_t)s;
+        }
+      }
+    }
+    const unsigned m1 = __ballot_sync(0xffffffffu, e1), m2 = __ballot_sync(0xffffffffu, e2);
+    const int tot = __popc(m1) + __popc(m2);
+    if (tot == 0) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(cursor, (unsigned long long)tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const unsigned lt = lanemask_lt();
+    if (e1) keys[base + __popc(m1 & lt)] = k1;
+    if (e2) keys[base + __popc(m1) + __popc(m2 & lt)] = k2;
+  }
+}
+
+// coarse arcs (cmap[v], cmap[u]) of a CSR, intra-cluster arcs dropped
+// (coarsen.py:200-253): per-cluster histogram, warp per vertex
+__global__ void mapped_hist_kernel(const int64_t *__restrict__ xadj,
+                                   const int32_t *__restrict__ adj,
+                                   const int32_t *__restrict__ cmap, int64_t V,
+                                   unsigned long long *__restrict__ hist) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < V; v += nwarps) {
+    const int32_t cv = cmap[v];
+    unsigned cnt = 0;
+    for (int64_t e = xadj[v] + lane; e < xadj[v + 1]; e += 32) cnt += cmap[adj[e]] != cv;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    if (lane == 0 && cnt) atomicAdd(hist + cv, (unsigned long long)cnt);
+  }
+}
+
+__global__ void mapped_keys_range_kernel(const int64_t *__restrict__ xadj,
+                                         const int32_t *__restrict__ adj,
+                                         const int32_t *__restrict__ cmap, int64_t V, int64_t c0,
+                                         int64_t c1, uint64_t nc, uint64_t *__restrict__ keys,
+                                         unsigned long long *__restrict__ cursor) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned lt = lanemask_lt();
+  for (int64_t v = warp; v < V; v += nwarps) {
+    const int64_t cv = cmap[v];
+    if (cv < c0 || cv >= c1) continue;  // warp-uniform
+    const int64_t e0 = xadj[v], e1 = xadj[v + 1];
+    for (int64_t eb = e0; eb < e1; eb += 32) {
+      const int64_t e = eb + lane;
+      int64_t cu = cv;
+      if (e < e1) cu = cmap[adj[e]];
+      const bool emit = cu != cv;
+      const unsigned m = __ballot_sync(0xffffffffu, emit);
+      if (!m) continue;
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(cursor, (unsigned long long)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (emit) keys[base + __popc(m & lt)] = (uint64_t)(cv - c0) * nc + (uint64_t)cu;
+    }
+  }
+}
+
+// rows [r0, r1) of xadj from the block's sorted unique keys (row-relative)
+__global__ void xadj_rows_from_keys(const uint64_t *__restrict__ keys, int64_t nkeys,
+                                    int64_t rows, uint64_t ncols, int64_t base,
+                                    int64_t *__restrict__ xadj_rows) {
+  GRID_STRIDE(r, rows) {
+    const uint64_t target = (uint64_t)r * ncols;
+    int64_t lo = 0, hi = nkeys;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < target)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    xadj_rows[r] = base + lo;
+  }
+}
+
+GB_API int gb_arc_histogram(const int64_t *src, const int64_t *dst, int64_t num_arcs,
+                            unsigned flags, int64_t *hist, void *stream_handle) {
+  GB_REQUIRE(num_arcs >= 0 && hist && (num_arcs == 0 || (src && dst)),
+             "gb_arc_histogram: bad args");
+  if (num_arcs == 0) return GB_OK;
+  arc_hist_kernel<<<blocks_for(num_arcs), 256, 0, as_stream(stream_handle)>>>(
+      src, dst, num_arcs, flags & GB_CSR_DROP_SELF, flags & GB_CSR_SYMMETRIZE,
+      reinterpret_cast<unsigned long long *>(hist));
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
+GB_API int gb_arc_keys_range(const int64_t *src, const int64_t *dst, int64_t num_arcs,
+                             unsigned flags, int64_t num_vertices, int64_t r0, int64_t r1,
+                             uint64_t *keys, int64_t *cursor, void *stream_handle) {
+  GB_REQUIRE(num_arcs >= 0 && keys && cursor && r0 >= 0 && r1 >= r0 && r1 <= num_vertices,
+             "gb_arc_keys_range: bad args");
+  if (num_arcs == 0 || r1 == r0) return GB_OK;
+  arc_keys_range_kernel<<<blocks_for(num_arcs), 256, 0, as_stream(stream_handle)>>>(
+      src, dst, num_arcs, flags & GB_CSR_DROP_SELF, flags & GB_CSR_SYMMETRIZE, r0, r1,
+      (uint64_t)num_vertices, keys, reinterpret_cast<unsigned long long *>(cursor));
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
+GB_API int gb_mapped_histogram(const int64_t *xadj, const int32_t *adj, int64_t num_vertices,
+                               const int32_t *cmap, int64_t *hist, void *stream_handle) {
+  GB_REQUIRE(num_vertices >= 1 && xadj && cmap && hist, "gb_mapped_histogram: bad args");
+  const int blocks = (int)std::min<int64_t>((num_vertices + 7) / 8, (int64_t)num_sms() * 16);
+  mapped_hist_kernel<<<std::max(blocks, 1), 256, 0, as_stream(stream_handle)>>>(
+      xadj, adj, cmap, num_vertices, reinterpret_cast<unsigned long long *>(hist));
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
+GB_API int gb_mapped_keys_range(const int64_t *xadj, const int32_t *adj, int64_t num_vertices,
+                                const int32_t *cmap, int64_t num_clusters, int64_t c0,
+                                int64_t c1, uint64_t *keys, int64_t *cursor,
+                                void *stream_handle) {
+  GB_REQUIRE(num_vertices >= 1 && xadj && cmap && keys && cursor && c0 >= 0 && c1 >= c0 &&
+                 c1 <= num_clusters,
+             "gb_mapped_keys_range: bad args");
+  if (c1 == c0) return GB_OK;
+  const int blocks = (int)std::min<int64_t>((num_vertices + 7) / 8, (int64_t)num_sms() * 16);
+  mapped_keys_range_kernel<<<std::max(blocks, 1), 256, 0, as_stream(stream_handle)>>>(
+      xadj, adj, cmap, num_vertices, c0, c1, (uint64_t)num_clusters, keys,
+      reinterpret_cast<unsigned long long *>(cursor));
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
+GB_API int gb_keys_to_rows_workspace(int64_t num_keys, int64_t rows, int64_t num_cols,
+                                     size_t *bytes) {
+  GB_REQUIRE(num_keys >= 0 && rows >= 1 && num_cols >= 1 && bytes,
+             "gb_keys_to_rows_workspace: bad args");
+  Carver c(nullptr);
+  KeyCsrBuffers b;
+  int rc = key_csr_carve(c, std::max<int64_t>(num_keys, 1),
+                         bits_for((uint64_t)rows * (uint64_t)num_cols), b);
+  if (rc) return rc;
+  *bytes = c.off + 256;
+  return GB_OK;
+}
+
+// Sort + deduplicate one block's keys and emit its rows: xadj_rows[0..rows)
+// (offset by `base`, the arcs of the earlier blocks) and adj_out[0..unique).
+// Synchronizes; *num_unique_out (host) sizes the next block's offset.
+GB_API int gb_keys_to_rows(uint64_t *keys, int64_t num_keys, int64_t rows, int64_t num_cols,
+                           int64_t base, int64_t *xadj_rows, int32_t *adj_out,
+                           int64_t *num_unique_out, void *workspace, size_t ws_bytes,
+                           void *stream_handle) {
+  GB_REQUIRE(num_keys >= 0 && rows >= 1 && num_cols >= 1 && xadj_rows && num_unique_out &&
+                 (num_keys == 0 || (keys && adj_out)),
+             "gb_keys_to_rows: bad args");
+  cudaStream_t st = as_stream(stream_handle);
+  Carver c(workspace);
+  KeyCsrBuffers b;
+  const int end_bit = bits_for((uint64_t)rows * (uint64_t)num_cols);
+  int rc = key_csr_carve(c, std::max<int64_t>(num_keys, 1), end_bit, b);
+  if (rc) return rc;
+  GB_REQUIRE(c.off <= ws_bytes, "gb_keys_to_rows: workspace too small");
+  int64_t nuniq = 0;
+  if (num_keys > 0) {
+    size_t tb = b.cub_bytes;
+    GB_CUDA_TRY(cub::DeviceRadixSort::SortKeys(b.cub_tmp, tb, keys, b.keys_alt, num_keys, 0,
+                                               end_bit, st));
+    tb = b.cub_bytes;
+    GB_CUDA_TRY(
+        cub::DeviceSelect::Unique(b.cub_tmp, tb, b.keys_alt, b.uniq, b.num_sel, num_keys, st));
+    GB_CUDA_TRY(cudaMemcpyAsync(&nuniq, b.num_sel, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    GB_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  xadj_rows_from_keys<<<blocks_for(rows), 256, 0, st>>>(b.uniq, nuniq, rows,
+                                                         (uint64_t)num_cols, base, xadj_rows);
+  GB_CHECK_LAUNCH();
+  if (nuniq > 0) {
+    adj_from_keys<<<blocks_for(nuniq), 256, 0, st>>>(b.uniq, nuniq, num_cols, adj_out);
+    GB_CHECK_LAUNCH();
+  }
+  GB_CUDA_TRY(cudaStreamSynchronize(st));
+  *num_unique_out = nuniq;
+  return GB_OK;
+}
+
+GB_API int gb_rmat_edges_range(int scale, int64_t first, int64_t count, double t_a, double t_ab,
+                               double t_abc, uint64_t seed, const int64_t *perm, int64_t *src,
+                               int64_t *dst, void *stream_handle) {
+  GB_REQUIRE(scale >= 1 && scale <= 34 && first >= 0 && count >= 0 && src && dst,
+             "gb_rmat_edges_range: bad args");
+  if (count == 0) return GB_OK;
+  rmat_range_kernel<<<blocks_for(count), 256, 0, as_stream(stream_handle)>>>(
+      scale, first, count, t_a, t_ab, t_abc, seed, perm, src, dst);
   GB_CHECK_LAUNCH();
   return GB_OK;
 }

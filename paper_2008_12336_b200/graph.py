@@ -198,6 +198,78 @@ def _csr_device(num_vertices: int, src: torch.Tensor, dst: torch.Tensor, flags: 
                  adj_dev=adj)
 
 
+def plan_row_blocks(hist: np.ndarray, max_block_keys: int) -> list[tuple[int, int]]:
+    """Consecutive row ranges whose arc counts (hist, an upper bound per row)
+    sum to at most max_block_keys; a row above the cap gets a block of its
+    own."""
+    if max_block_keys < 1:
+        raise ValueError("max_block_keys must be positive")
+    csum = np.concatenate([[0], np.cumsum(hist, dtype=np.int64)])
+    n = hist.shape[0]
+    blocks, r0 = [], 0
+    while r0 < n:
+        r1 = int(np.searchsorted(csum, csum[r0] + max_block_keys, side="right")) - 1
+        r1 = min(max(r1, r0 + 1), n)
+        blocks.append((r0, r1))
+        r0 = r1
+    return blocks
+
+
+def csr_from_blocks(num_rows: int, num_cols: int, hist: torch.Tensor, fill_block,
+                    max_block_keys: int, directed: bool = False, orig_ids=None) -> Graph:
+    """Row-block CSR construction (gb_keys_to_rows): rows are keyed, sorted,
+    deduplicated and emitted one block at a time, so scratch scales with
+    max_block_keys instead of the arc count.  `fill_block(r0, r1, keys,
+    cursor)` appends the keys of the block's arcs (gb_arc_keys_range /
+    gb_mapped_keys_range over every batch).  Equal to the one-shot build bit
+    for bit: blocks emit their rows in order."""
+    h = hist.cpu().numpy()
+    upper = int(h.sum())
+    blocks = plan_row_blocks(h, max_block_keys)
+    block_keys = int(max((h[a:b].sum() for a, b in blocks), default=0))
+    xadj = torch.empty(num_rows + 1, dtype=torch.int64, device="cuda")
+    adj = torch.empty(max(upper, 1), dtype=torch.int32, device="cuda")
+    keys = torch.empty(max(block_keys, 1), dtype=torch.int64, device="cuda")
+    cursor = torch.zeros(1, dtype=torch.int64, device="cuda")
+    rows_max = max((b - a for a, b in blocks), default=1)
+    ws, wsb = _lib.workspace("gb_keys_to_rows_workspace", max(block_keys, 1), rows_max, num_cols)
+    base = 0
+    for r0, r1 in blocks:
+        cursor.zero_()
+        fill_block(r0, r1, keys, cursor)
+        nk = int(cursor.item())
+        nu = C.c_int64(0)
+        _lib.call("gb_keys_to_rows", _lib.ptr(keys), nk, r1 - r0, num_cols, base,
+                  xadj.data_ptr() + r0 * 8, adj.data_ptr() + base * 4, C.byref(nu),
+                  _lib.ptr(ws), wsb, _lib.stream())
+        base += int(nu.value)
+    xadj[num_rows] = base
+    del ws, keys
+    adj = adj[: max(base, 1)].clone() if upper > 1.25 * max(base, 1) else adj
+    return Graph(num_rows, base, directed=directed, orig_ids=orig_ids, xadj_dev=xadj,
+                 adj_dev=adj)
+
+
+def csr_from_arc_batches(num_vertices: int, batches, flags: int, max_block_keys: int,
+                         directed: bool = False) -> Graph:
+    """from_edges semantics (graph.py:93-131) over arcs that arrive in batches
+    (`batches()` yields device (src, dst) int64 pairs and may be called once
+    per block, e.g. regenerating R-MAT samples), built block by block."""
+    _lib.require_cuda()
+    st = _lib.stream()
+    hist = torch.zeros(num_vertices, dtype=torch.int64, device="cuda")
+    for src, dst in batches():
+        _lib.call("gb_arc_histogram", _lib.ptr(src), _lib.ptr(dst), src.numel(), flags,
+                  _lib.ptr(hist), st)
+
+    def fill(r0, r1, keys, cursor):
+        for src, dst in batches():
+            _lib.call("gb_arc_keys_range", _lib.ptr(src), _lib.ptr(dst), src.numel(), flags,
+                      num_vertices, r0, r1, _lib.ptr(keys), _lib.ptr(cursor), st)
+
+    return csr_from_blocks(num_vertices, num_vertices, hist, fill, max_block_keys, directed)
+
+
 def array_checksum(t) -> int:
     """Position-keyed checksum of an int32/int64 array on the device
     (gb_checksum): sum_i mix64((i * 0x9E3779B97F4A7C15) ^ int64(x[i])) mod

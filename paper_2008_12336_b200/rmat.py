@@ -43,12 +43,46 @@ def rmat_edges(scale: int, num_samples: int, seed: int, permute: bool = True,
 
 
 def rmat_graph(scale: int, num_samples: int, seed: int = 7, densify_ids: bool = False,
-               permute: bool = True) -> Graph:
+               permute: bool = True, max_block_keys: int | None = None,
+               batch_samples: int = 1 << 28) -> Graph:
     """Undirected R-MAT CSR on the device.  With densify_ids, isolated ids
-    are dropped (orig_ids holds the surviving raw ids)."""
-    src, dst = rmat_edges(scale, num_samples, seed, permute)
-    g = _csr_device(1 << scale, src, dst, _lib.GB_CSR_DROP_SELF | _lib.GB_CSR_SYMMETRIZE, False)
-    del src, dst
+    are dropped (orig_ids holds the surviving raw ids).
+
+    max_block_keys: build the CSR block by block (graph.csr_from_arc_batches)
+    with samples regenerated in batches of batch_samples for every block
+    (each sample is a pure function of its index), so neither the sample
+    arrays nor the key scratch scale with the graph -- the path for graphs
+    whose one-shot build exceeds one GPU (C5).  Same graph bit for bit."""
+    flags = _lib.GB_CSR_DROP_SELF | _lib.GB_CSR_SYMMETRIZE
+    if max_block_keys is not None:
+        from .graph import csr_from_arc_batches
+        _lib.require_cuda()
+        a, b, c = RMAT_ABCD[:3]
+        perm = None
+        if permute:
+            ws, wsb = _lib.workspace("gb_rmat_permutation_workspace", scale)
+            perm = torch.empty(1 << scale, dtype=torch.int64, device="cuda")
+            _lib.call("gb_rmat_permutation", scale, _lib.u64(seed), _lib.ptr(perm),
+                      _lib.ptr(ws), wsb, _lib.stream())
+            del ws
+        bs = max(1, min(batch_samples, num_samples))
+        src = torch.empty(bs, dtype=torch.int64, device="cuda")
+        dst = torch.empty(bs, dtype=torch.int64, device="cuda")
+
+        def batches():
+            for first in range(0, num_samples, bs):
+                n = min(bs, num_samples - first)
+                _lib.call("gb_rmat_edges_range", scale, first, n, a, a + b, a + b + c,
+                          _lib.u64(seed), _lib.ptr(perm), _lib.ptr(src), _lib.ptr(dst),
+                          _lib.stream())
+                yield src[:n], dst[:n]
+
+        g = csr_from_arc_batches(1 << scale, batches, flags, max_block_keys)
+        del src, dst, perm
+    else:
+        src, dst = rmat_edges(scale, num_samples, seed, permute)
+        g = _csr_device(1 << scale, src, dst, flags, False)
+        del src, dst
     if densify_ids:
         g2, kept = densify(g)
         g2.orig_ids = kept

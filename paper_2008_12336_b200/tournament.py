@@ -46,7 +46,7 @@ import torch
 
 from . import _lib
 from .bigtrain import PairSides, PartitionPlan, _derived_seed, rotation_pairs
-from .errors import ConfigError
+from .errors import ConfigError, PlanError
 from .graph import Graph
 from .trainer import TrainConfig, lr_at
 
@@ -564,8 +564,17 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
             out.append((r, lst))
         return out
 
+    # Pools are drawn a round ahead (own buffer set per round parity and
+    # rank) when something can overlap them: the P2P shift between real
+    # ranks, or the other virtual ranks' streams.  Virtual ranks on one
+    # stream draw each pair's pools right before it (one shared buffer set).
+    ahead = has_prepare and (distributed or streams is not None)
+
+    def tag(ri, r, k):
+        return f"{ri % 2}.{r}.{k}." if ahead else f"x.{k}."
+
     def prepare(steps, ri):
-        if not has_prepare:
+        if not ahead:
             return
         for r, lst in steps:
             ctx = torch.cuda.stream(streams[r]) if streams else _null()
@@ -573,7 +582,7 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
                 if streams:
                     streams[r].wait_stream(main)
                 for k, s in lst:
-                    fns[r].prepare(s, f"{ri % 2}.{k}.")
+                    fns[r].prepare(s, tag(ri, r, k))
 
     for rot in range(rotations):
         arr = initial_arrangement(K)
@@ -590,7 +599,9 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
                     for k, s in lst:
                         Ma, Mb = store.pair_views(r, s.a, s.b)
                         if has_prepare:
-                            fns[r].train(Ma, Mb, s, f"{ri % 2}.{k}.")
+                            if not ahead:
+                                fns[r].prepare(s, tag(ri, r, k))
+                            fns[r].train(Ma, Mb, s, tag(ri, r, k))
                         else:
                             pair_fn(Ma, Mb, s)
                         n_pairs += 1
@@ -722,12 +733,39 @@ def sequential_order(K: int, rotations: int):
     return out
 
 
+def shard_plan(num_rows: int, dim: int, world: int, budget_bytes: int,
+               distributed: bool) -> tuple[int, int, bool]:
+    """Ranks of the schedule and part placement for a level under a per-GPU
+    byte budget for parts (MemoryBudget.resident_bytes): returns (G schedule
+    ranks, ranks per process, host_parts).
+
+    Device parts are preferred: a process holds 2 parts per schedule rank it
+    runs (+ 2 receive twins with real ranks).  When that exceeds the budget
+    the parts go to pinned host memory and only 4 device slots (+ twins)
+    stay, and K = 2G grows until those fit -- bigtrain.plan_partitions'
+    rule (bigtrain.py:133-149) applied per GPU."""
+    def part(G):
+        return -(-num_rows // (2 * G)) * dim * 4
+    twins = 2 if distributed else 0
+    G = world
+    if (2 * (1 if distributed else world) + twins) * part(world) <= budget_bytes:
+        return world, 1, False
+    m = 1
+    while (4 + twins) * part(world * m) > budget_bytes:
+        if 2 * world * m >= num_rows:
+            raise PlanError(f"budget {budget_bytes} B cannot hold 4 part slots of a "
+                            f"{num_rows}-row level")
+        m *= 2
+    G = world * m
+    return G, (m if distributed else G), True
+
+
 def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
                              shard_levels: int = 1, batch_size: int = 5, group=None,
                              num_ranks: int | None = None, hierarchy=None,
                              return_device: bool = False, balanced_pools: bool = True,
                              return_parts: bool = False, host_parts: bool = False,
-                             per_process: int = 1):
+                             per_process: int = 1, budget=None, no_coarsen: bool = False):
     """train_multilevel (trainer.py:252-288) with the finest `shard_levels`
     levels trained by the tournament across ranks.
 
@@ -744,21 +782,35 @@ def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
     Returns (matrix, per-level stats); with return_parts the finest level
     stays sharded and the first element is its PartStore (rows per rank).
 
+    budget (MemoryBudget): per-GPU bytes for the parts of the sharded levels
+    (shard_plan) -- beyond it parts go to pinned host memory and K grows;
+    the schedule is then planned from the finest level.
+
     balanced_pools (default; Hogwild runs only): the sharded levels draw
     balanced pools (TrainConfig.balanced_pools), which keeps this path's
     AUCROC at the in-memory pass's (C3: 0.823-0.829 vs 0.826) where the
     reference's fixed-B pools of train_large lose 0.04 (DESIGN.md 6);
     False keeps the reference's pools."""
-    from .coarsen import coarsen_all
+    from .coarsen import Hierarchy, coarsen_all
     from .trainer import epoch_plan, expand_embedding, init_embedding, train_level
     import torch.distributed as dist
     cfg.validate()
     if balanced_pools and not cfg.deterministic and not cfg.balanced_pools:
         cfg = dataclasses.replace(cfg, balanced_pools=True)
+    if budget is not None and shard_levels > 0:
+        world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) \
+            else (num_ranks or 1)
+        Gb, per_process, host_parts = shard_plan(
+            g0.num_vertices if hierarchy is None else hierarchy.graphs[0].num_vertices,
+            cfg.dim, world, budget.resident_bytes,
+            dist.is_available() and dist.is_initialized())
+        if not (dist.is_available() and dist.is_initialized()):
+            num_ranks = Gb
     distributed, G, local = _world(group, num_ranks, per_process)
     rank = dist.get_rank(group) if distributed else 0
     if hierarchy is None:
-        hierarchy = coarsen_all(g0, threshold=threshold)
+        hierarchy = (Hierarchy(graphs=[g0], mappings=[]) if no_coarsen
+                     else coarsen_all(g0, threshold=threshold))
     depth = hierarchy.depth
     # total_epochs == 0: the random-projection baseline, like train_multilevel
     plan = (np.zeros(depth, dtype=np.int64) if cfg.total_epochs == 0

@@ -91,3 +91,69 @@ def test_c1_aucroc_parity_with_reference(cuda):
     assert abs(ci["mean"]) <= AUC_TOL, msg
     assert -AUC_TOL <= ci["lo"] and ci["hi"] <= AUC_TOL, msg
     assert abs(np.mean(mine) - np.mean([runs[s] for s in seeds])) <= AUC_TOL, msg
+
+
+# -- row-block (chunked) graph construction: the C5 path -----------------------------
+@pytest.mark.parametrize("dens", [False, True])
+def test_blocked_rmat_csr_equals_one_shot(cuda, dens):
+    """The row-block CSR build (bounded key scratch, samples regenerated per
+    block) equals the one-shot build bit for bit."""
+    a = gb.rmat_graph(16, 1 << 20, 3, densify_ids=dens)
+    for cap, batch in [(1 << 18, 1 << 18), (50_000, 300_000)]:
+        b = gb.rmat_graph(16, 1 << 20, 3, densify_ids=dens, max_block_keys=cap,
+                          batch_samples=batch)
+        assert (a.num_vertices, a.num_edges) == (b.num_vertices, b.num_edges)
+        assert np.array_equal(a.xadj, b.xadj) and np.array_equal(a.adj, b.adj)
+
+
+def test_blocked_arc_batches_equal_from_edges(cuda):
+    import torch
+    from paper_2008_12336_b200 import _lib
+    from paper_2008_12336_b200.graph import csr_from_arc_batches
+    rng = np.random.default_rng(4)
+    V = 5000
+    e = rng.integers(0, V, size=(60_000, 2))
+    e[:50, 1] = e[:50, 0]  # self-loops dropped
+    ref = gb.from_edges(e, num_vertices=V)
+    t = torch.from_numpy(e).cuda()
+
+    def batches():
+        for i in range(0, e.shape[0], 7_000):
+            yield t[i:i + 7_000, 0].contiguous(), t[i:i + 7_000, 1].contiguous()
+
+    got = csr_from_arc_batches(V, batches, _lib.GB_CSR_DROP_SELF | _lib.GB_CSR_SYMMETRIZE,
+                               max_block_keys=9_000)
+    assert np.array_equal(got.xadj, ref.xadj) and np.array_equal(got.adj, ref.adj)
+
+
+def test_blocked_coarsening_equals_one_shot(cuda, orc):
+    g = gb.rmat_graph(16, 1 << 20, 5, densify_ids=True)
+    h1 = gb.coarsen_all(g, threshold=100)
+    h2 = gb.coarsen_all(g, threshold=100, max_block_keys=100_000)
+    assert h1.depth == h2.depth
+    for L in range(h1.depth):
+        assert np.array_equal(h1.graphs[L].xadj, h2.graphs[L].xadj), L
+        assert np.array_equal(h1.graphs[L].adj, h2.graphs[L].adj), L
+
+
+def test_c5_path_under_a_per_gpu_budget(cuda, orc):
+    """C5 at reduced scale: a level built block by block under a key budget,
+    then trained by the sharded path under a per-GPU byte budget far below the
+    matrix -- parts in pinned host memory, K grown until four device slots
+    fit (shard_plan) -- with the same result as the unbudgeted tournament at
+    that K (deterministic kernels)."""
+    from paper_2008_12336_b200 import tournament as tn
+    g = gb.rmat_graph(13, 1 << 16, 9, max_block_keys=20_000)
+    d = 32
+    cfg = gb.TrainConfig(dim=d, total_epochs=4, negative_samples=3, seed=2,
+                         deterministic=True)
+    M_bytes = g.num_vertices * d * 4
+    budget = gb.MemoryBudget(resident_bytes=M_bytes // 6)
+    G, per_proc, host = tn.shard_plan(g.num_vertices, d, 1, budget.resident_bytes, False)
+    assert host and G >= 8
+    store, _ = gb.train_multilevel_sharded(g, cfg, no_coarsen=True, budget=budget,
+                                           return_parts=True)
+    assert store.host and store.G == G
+    assert store.device_bytes <= budget.resident_bytes
+    ref, _ = gb.train_multilevel_sharded(g, cfg, no_coarsen=True, num_ranks=G)
+    assert np.array_equal(store.to_full().cpu().numpy(), ref)
