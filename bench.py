@@ -640,8 +640,8 @@ def run_sharded_reference(args):
 
 def run_tournament(args):
     """Part-pair tournament (tournament.py) on the C2 graph: K = 2N parts,
-    one step = one rotation (every pair once, K(K+1)/2 pair launches per
-    rotation, parts exchanged over NCCL between rounds).  Units: positive +
+    one step = --rotations rotations (every pair once per rotation, K(K+1)/2
+    pair launches, parts exchanged over NCCL between rounds).  Units: positive +
     negative updates, B=5 positives per source per pair side."""
     import torch
     rank, world, local = dist_init()
@@ -657,9 +657,12 @@ def run_tournament(args):
     M = torch.from_numpy(gb.init_embedding(V, dim, 1)).to(dev)
 
     vr = max(1, args.virtual_ranks)
+    K = 2 * world if world > 1 else 2 * vr
+    R = max(1, args.rotations)
 
     def step():
-        return tn.train_tournament(G, M, cfg, 1, batch_size=B, gather=False,
+        # an R * B * K vertex-pass budget = R rotations (tournament_rotations)
+        return tn.train_tournament(G, M, cfg, R * B * K, batch_size=B, gather=False,
                                    num_ranks=None if world > 1 else vr)
 
     for _ in range(args.warmup):
@@ -687,7 +690,6 @@ def run_tournament(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     value = upd / (total_ms / 1000.0)  # pos_updates are already summed over ranks
-    K = 2 * world if world > 1 else 2 * vr
     bpu = 8 * dim + (8 * dim) / (B * (1 + NNEG))
     peak, peak_src = measured_peak()
     line = {
@@ -698,7 +700,9 @@ def run_tournament(args):
         "config": workload_config({
             "workload": f"part-pair tournament on the C2 graph, K={K} parts, B={B}, d={dim}",
             "dim": dim,
-            "step": "one rotation: K(K+1)/2 pairs, K-1 part exchanges",
+            "step": f"{R} rotations: each K(K+1)/2 pairs, K-1 part exchanges "
+                    "(one process: rotation 0 eager, the rest replayed from a CUDA graph)",
+            "rotation_graph": os.environ.get("GB_ROTATION_GRAPH", "1") != "0",
             "parallelism": f"tournament over {world} GPU(s)"
                            + (f" ({vr} virtual ranks)" if world == 1 and vr > 1 else ""),
             "vertices": V, "pool_mode": os.environ.get("GB_POOL_MODE", "compact")}),
@@ -732,6 +736,8 @@ def main():
                          "strong scaling)")
     ap.add_argument("--dim", type=int, default=0,
                     help="tournament workload: embedding dimension (default 128; C5 uses 256)")
+    ap.add_argument("--rotations", type=int, default=8,
+                    help="tournament workload: rotations per step")
     ap.add_argument("--virtual-ranks", type=int, default=1,
                     help="tournament on one GPU: run the schedule of R ranks (K = 2R parts) "
                          "in this process")

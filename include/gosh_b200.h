@@ -161,6 +161,19 @@ int gb_collapse(int64_t num_vertices, const int64_t *xadj, const int64_t *in_xad
                 int64_t *num_clusters_out, int *rounds_out, void *workspace,
                 size_t ws_bytes, void *stream_handle);
 
+/* run-dependent parallel collapse: the reference's try-lock mode
+ * (coarsen.py:117-179 _collapse_par + _normalize; collapse_map_parallel).
+ * num_workers warps grab GRAB_BATCH=64 order positions at a time, claim hubs
+ * and members with CAS and skip on a lost race; hubs are renumbered by order
+ * position.  num_workers=1 equals gb_collapse; more workers give a valid,
+ * interleaving-dependent map (not in the parity contract, coarsen.py:11-13).
+ * xadj/adj is the out-arc CSR, as in the reference.  Synchronizes. */
+int gb_collapse_cas_workspace(int64_t num_vertices, size_t *bytes);
+int gb_collapse_cas(int64_t num_vertices, const int64_t *xadj, const int32_t *adj,
+                    const int64_t *order, double delta, int64_t num_workers, int32_t *cmap,
+                    int64_t *num_clusters_out, void *workspace, size_t ws_bytes,
+                    void *stream_handle);
+
 /* coarse CSR: row c = sorted unique {map[u] : u in N(members of c)} \ {c}
  * (coarsen.py:182-281 build_coarse_graph).  adj_out must hold num_edges
  * entries.  Synchronizes; writes the coarse arc count. */
@@ -361,6 +374,74 @@ int gb_auc_roc_workspace(int64_t n, size_t *bytes);
 int gb_auc_roc(const double *scores, const int8_t *labels, int64_t n,
                unsigned long long *rank2_pos, void *workspace,
                size_t workspace_bytes, void *stream_handle);
+
+/* ---- device-parameter forms for CUDA-graph replay -------------------------
+ * gb_fill_pool_side / gb_train_pool_side / gb_fill_pool_compact /
+ * gb_train_pool_list / gb_fill_pool_balanced / gb_train_pool_balanced with the pair's seed and lr read at run time from
+ * `param`, a device pointer to {uint64 seed; double lr;} (16 bytes), instead
+ * of the scalar arguments.  A rotation of the part-pair tournament is the
+ * same launch sequence every time except for these two values, so it is
+ * captured once into a CUDA graph and replayed with a rewritten parameter
+ * table (tournament.py).  Results equal the scalar forms. */
+int gb_fill_pool_side_dp(const int64_t *xadj, const int32_t *adj, int64_t lo_s, int64_t hi_s,
+                         int64_t lo_t, int64_t hi_t, int B, const void *param, uint64_t side,
+                         int32_t *out, void *stream_handle);
+int gb_train_pool_side_dp(float *Msrc, float *Mtgt, int dim, const int32_t *targets,
+                          int64_t n_src, int B, int64_t lo_t, int64_t n_t, int n_neg,
+                          const void *param, uint64_t side, const int64_t *xadj,
+                          const int32_t *adj, int64_t lo_s, uint64_t pool_side, unsigned flags,
+                          int64_t max_groups, int64_t *status, void *stream_handle);
+int gb_fill_pool_compact_dp(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
+                            int64_t hi_s, int64_t lo_t, int64_t hi_t, int B, const void *param,
+                            uint64_t side, int32_t *list, int32_t *targets, int64_t *count,
+                            void *stream_handle);
+int gb_train_pool_list_dp(float *Msrc, float *Mtgt, int dim, const int32_t *list,
+                          const int32_t *targets, const int64_t *count, int64_t max_src, int B,
+                          int64_t lo_t, int64_t n_t, int n_neg, const void *param, uint64_t side,
+                          unsigned flags, int64_t max_groups, int64_t *status,
+                          void *stream_handle);
+int gb_fill_pool_balanced_dp(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
+                             int64_t hi_s, int64_t lo_t, int64_t hi_t, int64_t BK,
+                             const void *param, uint64_t side, int32_t *list, int64_t *first,
+                             int32_t *cnt, int32_t *npos, int64_t *count, void *stream_handle);
+int gb_train_pool_balanced_dp(float *Msrc, float *Mtgt, int dim, const int32_t *list,
+                              const int64_t *first, const int32_t *cnt, const int32_t *npos,
+                              const int64_t *count, int64_t max_src, int B, int64_t lo_t,
+                              int64_t n_t, int n_neg, const void *param, uint64_t side,
+                              const int32_t *adj, int64_t lo_s, uint64_t pool_side,
+                              unsigned flags, int64_t max_groups, int64_t *status,
+                              void *stream_handle);
+
+/* ---- graph input on the device --------------------
+ * CSR validation of a loaded GSHG file (graph.py:61-77 Graph.validate, run by
+ * load_graph, graph.py:203-219).  *flags_out (host) gets a bit per failed
+ * check, in the reference's order: 1 xadj endpoints, 2 xadj decreasing, 4 adj
+ * entry out of range, 8 a row not strictly ascending (meaningful only when 1
+ * and 2 are clear).  Synchronizes. */
+int gb_csr_validate_workspace(int64_t num_edges, size_t *bytes);
+int gb_csr_validate(int64_t num_vertices, int64_t num_edges, const int64_t *xadj,
+                    const int32_t *adj, int *flags_out, void *workspace, size_t ws_bytes,
+                    void *stream_handle);
+
+/* Edge-list text (graph.py:134-157 load_edge_list's loop) in device memory:
+ * lines end at '\n'; blank and '#' lines are skipped; a line must hold two
+ * fields that Python's int() accepts ([+-]?digits with single underscores
+ * between digits).  u_out/v_out (room for num_bytes/2+1 entries) receive the
+ * ids of the edge lines in order.  result (host, 4 x int64): edges, lines,
+ * index of the first malformed line (-1 if none), 1 if a syntactically valid
+ * id lies outside int64 (the reference's later OverflowError).  ASCII text
+ * only (the caller routes other text to the host parser).  Synchronizes. */
+int gb_parse_edge_text_workspace(int64_t num_bytes, size_t *bytes);
+int gb_parse_edge_text(const char *text, int64_t num_bytes, int64_t *u_out, int64_t *v_out,
+                       int64_t *result, void *workspace, size_t ws_bytes,
+                       void *stream_handle);
+
+/* Id densification (graph.py:160-164: np.unique, then np.searchsorted):
+ * uniq (n entries of room) gets the sorted distinct values of ids; with
+ * relabel, ids[i] becomes its rank in uniq.  Synchronizes. */
+int gb_unique_ids_workspace(int64_t n, size_t *bytes);
+int gb_unique_ids(int64_t *ids, int64_t n, int64_t *uniq, int64_t *num_unique_out,
+                  int relabel, void *workspace, size_t ws_bytes, void *stream_handle);
 
 #ifdef __cplusplus
 }

@@ -50,6 +50,8 @@ SIGNATURES = {
     "gb_degree_order": (_int, [_i64, _p, _p, _p, _sz, _p]),
     "gb_collapse_workspace": (_int, [_i64, _psz]),
     "gb_collapse": (_int, [_i64, _p, _p, _p, _p, _dbl, _p, _pi64, _pint, _p, _sz, _p]),
+    "gb_collapse_cas_workspace": (_int, [_i64, _psz]),
+    "gb_collapse_cas": (_int, [_i64, _p, _p, _p, _dbl, _i64, _p, _pi64, _p, _sz, _p]),
     "gb_coarse_csr_workspace": (_int, [_i64, _i64, _i64, _psz]),
     "gb_coarse_csr": (_int, [_i64, _i64, _p, _p, _p, _i64, _p, _p, _pi64, _p, _sz, _p]),
     "gb_expand": (_int, [_p, _i64, _int, _p, _i64, _p, _p]),
@@ -61,6 +63,12 @@ SIGNATURES = {
     "gb_keys_to_rows_workspace": (_int, [_i64, _i64, _i64, _psz]),
     "gb_keys_to_rows": (_int, [_p, _i64, _i64, _i64, _i64, _p, _p, _pi64, _p, _sz, _p]),
     "gb_rmat_edges_range": (_int, [_int, _i64, _i64, _dbl, _dbl, _dbl, _u64, _p, _p, _p, _p]),
+    "gb_csr_validate_workspace": (_int, [_i64, _psz]),
+    "gb_csr_validate": (_int, [_i64, _i64, _p, _p, _pint, _p, _sz, _p]),
+    "gb_parse_edge_text_workspace": (_int, [_i64, _psz]),
+    "gb_parse_edge_text": (_int, [_p, _i64, _p, _p, _pi64, _p, _sz, _p]),
+    "gb_unique_ids_workspace": (_int, [_i64, _psz]),
+    "gb_unique_ids": (_int, [_p, _i64, _p, _pi64, _int, _p, _sz, _p]),
     "gb_train_passes": (_int, [_i64, _p, _p, _p, _i64, _p, _int, _int, _u64, _u64, _i64, _i64,
                                _i64, _p, C.c_uint, _i64, _p, _p]),
     "gb_active_sources_workspace": (_int, [_i64, _psz]),
@@ -80,6 +88,18 @@ SIGNATURES = {
     "gb_train_pool_balanced": (_int, [_p, _p, _int, _p, _p, _p, _p, _p, _i64, _int, _i64,
                                       _i64, _int, _dbl, _u64, _u64, _p, _i64, _u64, C.c_uint,
                                       _i64, _p, _p]),
+    "gb_fill_pool_side_dp": (_int, [_p, _p, _i64, _i64, _i64, _i64, _int, _p, _u64, _p, _p]),
+    "gb_train_pool_side_dp": (_int, [_p, _p, _int, _p, _i64, _int, _i64, _i64, _int, _p, _u64,
+                                     _p, _p, _i64, _u64, C.c_uint, _i64, _p, _p]),
+    "gb_fill_pool_compact_dp": (_int, [_p, _p, _i64, _i64, _i64, _i64, _int, _p, _u64, _p, _p,
+                                       _p, _p]),
+    "gb_train_pool_list_dp": (_int, [_p, _p, _int, _p, _p, _p, _i64, _int, _i64, _i64, _int, _p,
+                                     _u64, C.c_uint, _i64, _p, _p]),
+    "gb_fill_pool_balanced_dp": (_int, [_p, _p, _i64, _i64, _i64, _i64, _i64, _p, _u64, _p,
+                                        _p, _p, _p, _p, _p]),
+    "gb_train_pool_balanced_dp": (_int, [_p, _p, _int, _p, _p, _p, _p, _p, _i64, _int, _i64,
+                                         _i64, _int, _p, _u64, _p, _i64, _u64, C.c_uint,
+                                         _i64, _p, _p]),
     "gb_host_register": (_int, [_p, _sz]),
     "gb_host_unregister": (_int, [_p]),
     "gb_undirected_pairs_workspace": (_int, [_i64, _psz]),

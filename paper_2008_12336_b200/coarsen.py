@@ -146,13 +146,38 @@ def collapse_map(g: Graph, order) -> Mapping:
     return _collapse_dev(g, order)[0]
 
 
-def collapse_map_parallel(g: Graph, order, num_workers: int) -> Mapping:
-    """Reference signature of the parallel collapse (coarsen.py:166-179).  The
-    device collapse is already parallel and deterministic, so every worker
-    count returns the sequential result (which the reference guarantees only
-    for num_workers=1)."""
+def _collapse_cas_dev(g: Graph, order, num_workers: int) -> Mapping:
+    xadj, adj = g.device_csr()
+    V = g.num_vertices
+    if isinstance(order, torch.Tensor):
+        order_t = order.to(device="cuda", dtype=torch.int64).contiguous()
+    else:
+        order_t = torch.from_numpy(np.ascontiguousarray(order, dtype=np.int64)).cuda()
+    ws, wsb = _lib.workspace("gb_collapse_cas_workspace", V)
+    cmap = torch.empty(V, dtype=torch.int32, device="cuda")
+    nc = C.c_int64(0)
+    _lib.call("gb_collapse_cas", V, _lib.ptr(xadj), _lib.ptr(adj), _lib.ptr(order_t),
+              g.num_edges / g.num_vertices, int(num_workers), _lib.ptr(cmap), C.byref(nc),
+              _lib.ptr(ws), wsb, _lib.stream())
+    return Mapping(num_clusters=int(nc.value), map_dev=cmap)
+
+
+def collapse_map_parallel(g: Graph, order, num_workers: int,
+                          run_dependent: bool = False) -> Mapping:
+    """Reference signature of the parallel collapse (coarsen.py:166-179).
+
+    Default: the device collapse, which is parallel AND deterministic, so
+    every worker count returns the sequential result (the reference
+    guarantees that only for num_workers=1).  run_dependent=True runs the
+    reference's own try-lock algorithm (_collapse_par: CAS claims,
+    skip-on-failure, hubs renumbered by order position) with num_workers
+    concurrent warps (gb_collapse_cas): one worker equals collapse_map, more
+    give a valid map that depends on the interleaving -- the reference's
+    speed mode, outside its parity contract (coarsen.py:11-13)."""
     if num_workers < 1:
         raise ConfigError("num_workers must be >= 1")
+    if run_dependent:
+        return _collapse_cas_dev(g, order, num_workers)
     return collapse_map(g, order)
 
 
@@ -191,11 +216,14 @@ def build_coarse_graph(g: Graph, m: Mapping, num_workers: int = 1,
 
 
 def coarsen_all(g: Graph, threshold: int = 100, num_workers: int = 1,
-                max_block_keys: int | None = None) -> Hierarchy:
+                max_block_keys: int | None = None, run_dependent: bool = False) -> Hierarchy:
     """order -> collapse -> contract until |V| <= threshold; a level keeping
     more than 99% of the vertices is discarded and flags a stall
     (coarsen.py:284-311).  num_workers is accepted for API parity;
-    max_block_keys bounds the coarse-CSR key scratch (build_coarse_graph)."""
+    max_block_keys bounds the coarse-CSR key scratch (build_coarse_graph).
+    run_dependent with num_workers > 1 collapses with the reference's
+    try-lock mode (collapse_map_parallel, coarsen.py:299-302); the default is
+    the deterministic device collapse for every worker count."""
     if threshold < 1:
         raise ConfigError("threshold must be >= 1")
     if num_workers < 1:
@@ -206,7 +234,10 @@ def coarsen_all(g: Graph, threshold: int = 100, num_workers: int = 1,
         cur = graphs[-1]
         t0 = time.perf_counter()
         order = _degree_order_dev(cur)
-        m, r = _collapse_dev(cur, order)
+        if run_dependent and num_workers > 1:
+            m, r = _collapse_cas_dev(cur, order, num_workers), 1
+        else:
+            m, r = _collapse_dev(cur, order)
         if m.num_clusters > STALL_RATIO * cur.num_vertices:
             stalled = True
             break

@@ -1112,3 +1112,139 @@ GB_API int gb_rmat_edges_range(int scale, int64_t first, int64_t count, double t
   GB_CHECK_LAUNCH();
   return GB_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Run-dependent parallel collapse (coarsen.py:117-179 _collapse_par +
+// _normalize): the reference's try-lock/skip-on-failure mode, not part of the
+// parity contract.  A worker is one warp: it grabs kGrab consecutive order
+// positions from a shared cursor (GRAB_BATCH, coarsen.py:30), claims each
+// vertex as a hub with a CAS (provisional cluster id = its own id) and
+// offers its eligible neighbours to the hub with a CAS each (the lanes take
+// the row 32 arcs at a time: distinct u, so lane order is irrelevant); a
+// lost CAS skips the vertex, as the reference does.  One worker reproduces
+// the sequential collapse exactly; more workers give a valid map that
+// depends on the interleaving.  Normalisation numbers hubs by their order
+// position (flag + exclusive scan), like _normalize.
+// ---------------------------------------------------------------------------
+static constexpr int kGrab = 64;  // coarsen.py:30 GRAB_BATCH
+
+__global__ void collapse_cas_kernel(const int64_t *__restrict__ xadj,
+                                    const int32_t *__restrict__ adj,
+                                    const int64_t *__restrict__ order, int64_t V, double delta,
+                                    int32_t *cmap, unsigned long long *cursor) {
+  const int lane = threadIdx.x & 31;
+  volatile int32_t *vmap = cmap;
+  for (;;) {
+    unsigned long long lo = 0;
+    if (lane == 0) lo = atomicAdd(cursor, (unsigned long long)kGrab);
+    lo = __shfl_sync(0xffffffffu, lo, 0);
+    if ((int64_t)lo >= V) break;
+    const int64_t hi = min((int64_t)lo + kGrab, V);
+    for (int64_t i = (int64_t)lo; i < hi; ++i) {
+      const int64_t v = order[i];
+      int claimed = 0;
+      if (lane == 0) claimed = atomicCAS(cmap + v, -1, (int32_t)v) == -1;
+      if (!__shfl_sync(0xffffffffu, claimed, 0)) continue;
+      const int64_t b = xadj[v], e = xadj[v + 1];
+      const bool v_small = (double)(e - b) <= delta;  // coarsen.py:108
+      for (int64_t k = b + lane; k < e; k += 32) {
+        const int32_t u = adj[k];
+        if (vmap[u] != -1) continue;
+        if (v_small || (double)(xadj[u + 1] - xadj[u]) <= delta)  // coarsen.py:111
+          atomicCAS(cmap + u, -1, (int32_t)v);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void cas_hub_flags(const int64_t *__restrict__ order, const int32_t *__restrict__ cmap,
+                              int64_t V, int64_t *__restrict__ flag) {
+  GRID_STRIDE(i, V) {
+    const int64_t v = order[i];
+    flag[i] = cmap[v] == (int32_t)v ? 1 : 0;
+  }
+}
+
+__global__ void cas_dense_ids(const int64_t *__restrict__ order, const int64_t *__restrict__ flag,
+                              const int64_t *__restrict__ cid, int64_t V,
+                              int32_t *__restrict__ dense) {
+  GRID_STRIDE(i, V) if (flag[i]) dense[order[i]] = (int32_t)cid[i];
+}
+
+__global__ void cas_normalize(const int32_t *__restrict__ prov, const int32_t *__restrict__ dense,
+                              int64_t V, int32_t *__restrict__ out) {
+  GRID_STRIDE(v, V) out[v] = dense[prov[v]];
+}
+
+static int collapse_cas_layout(Carver &c, int64_t V, unsigned long long **cursor, int32_t **prov,
+                        int32_t **dense, int64_t **flag, int64_t **cid, void **tmp,
+                        size_t *tb) {
+  *cursor = c.take<unsigned long long>(1);
+  *prov = c.take<int32_t>(V);
+  *dense = c.take<int32_t>(V);
+  *flag = c.take<int64_t>(V + 1);
+  *cid = c.take<int64_t>(V + 1);
+  *tb = 0;
+  GB_CUDA_TRY(
+      cub::DeviceScan::ExclusiveSum(nullptr, *tb, (int64_t *)nullptr, (int64_t *)nullptr, V + 1));
+  *tmp = c.take_bytes(*tb);
+  return GB_OK;
+}
+GB_API int gb_collapse_cas_workspace(int64_t num_vertices, size_t *bytes) {
+  GB_REQUIRE(num_vertices >= 1 && num_vertices < (int64_t)INT32_MAX && bytes,
+             "gb_collapse_cas_workspace: bad args");
+  Carver c(nullptr);
+  unsigned long long *cur;
+  int32_t *p, *d;
+  int64_t *f, *cid;
+  void *tmp;
+  size_t tb;
+  int rc = collapse_cas_layout(c, num_vertices, &cur, &p, &d, &f, &cid, &tmp, &tb);
+  if (rc) return rc;
+  *bytes = c.off + 256;
+  return GB_OK;
+}
+
+GB_API int gb_collapse_cas(int64_t num_vertices, const int64_t *xadj, const int32_t *adj,
+                           const int64_t *order, double delta, int64_t num_workers,
+                           int32_t *cmap, int64_t *num_clusters_out, void *workspace,
+                           size_t ws_bytes, void *stream_handle) {
+  GB_REQUIRE(num_vertices >= 1 && num_vertices < (int64_t)INT32_MAX && xadj && adj && order &&
+                 cmap && num_clusters_out && num_workers >= 1,
+             "gb_collapse_cas: bad args");
+  const int64_t V = num_vertices;
+  cudaStream_t st = as_stream(stream_handle);
+  Carver c(workspace);
+  unsigned long long *cursor;
+  int32_t *prov, *dense;
+  int64_t *flag, *cid;
+  void *tmp;
+  size_t tb;
+  int rc = collapse_cas_layout(c, V, &cursor, &prov, &dense, &flag, &cid, &tmp, &tb);
+  if (rc) return rc;
+  GB_REQUIRE(c.off <= ws_bytes, "gb_collapse_cas: workspace too small");
+  GB_CUDA_TRY(cudaMemsetAsync(prov, 0xff, V * sizeof(int32_t), st));
+  GB_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), st));
+  // workers = warps; never more than there are batches to grab
+  const int64_t batches = (V + kGrab - 1) / kGrab;
+  const int64_t warps = std::min<int64_t>(std::min<int64_t>(num_workers, batches),
+                                          (int64_t)num_sms() * 64);
+  const int wpb = (int)std::min<int64_t>(warps, 8);
+  const int blocks = (int)((warps + wpb - 1) / wpb);
+  collapse_cas_kernel<<<blocks, wpb * 32, 0, st>>>(xadj, adj, order, V, delta, prov, cursor);
+  GB_CHECK_LAUNCH();
+  cas_hub_flags<<<blocks_for(V), 256, 0, st>>>(order, prov, V, flag);
+  GB_CHECK_LAUNCH();
+  GB_CUDA_TRY(cudaMemsetAsync(flag + V, 0, sizeof(int64_t), st));
+  GB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, flag, cid, V + 1, st));
+  cas_dense_ids<<<blocks_for(V), 256, 0, st>>>(order, flag, cid, V, dense);
+  GB_CHECK_LAUNCH();
+  cas_normalize<<<blocks_for(V), 256, 0, st>>>(prov, dense, V, cmap);
+  GB_CHECK_LAUNCH();
+  int64_t nc = 0;
+  GB_CUDA_TRY(cudaMemcpyAsync(&nc, cid + V, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GB_CUDA_TRY(cudaStreamSynchronize(st));
+  *num_clusters_out = nc;
+  return GB_OK;
+}

@@ -247,12 +247,12 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
   return GB_OK;
 }
 
-GB_API int gb_train_pool_side(float *Msrc, float *Mtgt, int dim, const int32_t *targets,
-                                  int64_t n_src, int B, int64_t lo_t, int64_t n_t, int n_neg,
-                                  double lr, uint64_t seed, uint64_t side, const int64_t *xadj,
-                                  const int32_t *adj, int64_t lo_s, uint64_t pool_side,
-                                  unsigned flags, int64_t max_groups, int64_t *status,
-                                  void *stream_handle) {
+static int train_pool_side_impl(float *Msrc, float *Mtgt, int dim, const int32_t *targets,
+                                int64_t n_src, int B, int64_t lo_t, int64_t n_t, int n_neg,
+                                double lr, uint64_t seed, uint64_t side, const int64_t *xadj,
+                                const int32_t *adj, int64_t lo_s, uint64_t pool_side,
+                                unsigned flags, int64_t max_groups, int64_t *status,
+                                const PairParam *param, void *stream_handle) {
   GB_REQUIRE(dim >= 1 && B >= 1 && n_neg >= 0 && n_src >= 0 && n_t >= 0,
              "gb_train_pool_side: bad sizes");
   GB_REQUIRE(Msrc && Mtgt && status, "gb_train_pool_side: null pointer");
@@ -265,7 +265,7 @@ GB_API int gb_train_pool_side(float *Msrc, float *Mtgt, int dim, const int32_t *
   select_hot(var, flags, Msrc == Mtgt, targets != nullptr);
   PoolArgs a{Msrc, Mtgt, dim, targets, n_src, B, lo_t, n_t, n_neg, lr, seed, side, xadj, adj,
              lo_s, pool_side, nullptr, nullptr, nullptr, nullptr, nullptr, (flags & GB_TRAIN_REUSE) != 0,
-             (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status};
+             (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status, param};
   int grid = 1;
   if (!exact) {
     int rc = grid_for((const void *)var.pool, var.G, max_groups, n_src, &grid, s0_bytes(var, dim));
@@ -274,11 +274,34 @@ GB_API int gb_train_pool_side(float *Msrc, float *Mtgt, int dim, const int32_t *
   return launch_pool(var, a, grid, as_stream(stream_handle));
 }
 
-GB_API int gb_train_pool_list(float *Msrc, float *Mtgt, int dim, const int32_t *list,
-                              const int32_t *targets, const int64_t *count, int64_t max_src,
-                              int B, int64_t lo_t, int64_t n_t, int n_neg, double lr,
-                              uint64_t seed, uint64_t side, unsigned flags, int64_t max_groups,
-                              int64_t *status, void *stream_handle) {
+GB_API int gb_train_pool_side(float *Msrc, float *Mtgt, int dim, const int32_t *targets,
+                              int64_t n_src, int B, int64_t lo_t, int64_t n_t, int n_neg,
+                              double lr, uint64_t seed, uint64_t side, const int64_t *xadj,
+                              const int32_t *adj, int64_t lo_s, uint64_t pool_side,
+                              unsigned flags, int64_t max_groups, int64_t *status,
+                              void *stream_handle) {
+  return train_pool_side_impl(Msrc, Mtgt, dim, targets, n_src, B, lo_t, n_t, n_neg, lr, seed,
+                              side, xadj, adj, lo_s, pool_side, flags, max_groups, status,
+                              nullptr, stream_handle);
+}
+
+GB_API int gb_train_pool_side_dp(float *Msrc, float *Mtgt, int dim, const int32_t *targets,
+                                 int64_t n_src, int B, int64_t lo_t, int64_t n_t, int n_neg,
+                                 const void *param, uint64_t side, const int64_t *xadj,
+                                 const int32_t *adj, int64_t lo_s, uint64_t pool_side,
+                                 unsigned flags, int64_t max_groups, int64_t *status,
+                                 void *stream_handle) {
+  GB_REQUIRE(param, "gb_train_pool_side_dp: null param");
+  return train_pool_side_impl(Msrc, Mtgt, dim, targets, n_src, B, lo_t, n_t, n_neg, 0.0, 0,
+                              side, xadj, adj, lo_s, pool_side, flags, max_groups, status,
+                              static_cast<const PairParam *>(param), stream_handle);
+}
+
+static int train_pool_list_impl(float *Msrc, float *Mtgt, int dim, const int32_t *list,
+                                const int32_t *targets, const int64_t *count, int64_t max_src,
+                                int B, int64_t lo_t, int64_t n_t, int n_neg, double lr,
+                                uint64_t seed, uint64_t side, unsigned flags, int64_t max_groups,
+                                int64_t *status, const PairParam *param, void *stream_handle) {
   GB_REQUIRE(dim >= 1 && B >= 1 && n_neg >= 0 && max_src >= 0 && n_t >= 0,
              "gb_train_pool_list: bad sizes");
   GB_REQUIRE(Msrc && Mtgt && status && list && targets && count,
@@ -292,7 +315,7 @@ GB_API int gb_train_pool_list(float *Msrc, float *Mtgt, int dim, const int32_t *
   PoolArgs a{Msrc, Mtgt, dim, targets, max_src, B, lo_t, n_t, n_neg, lr, seed, side, nullptr,
              nullptr, 0, 0, list, count, nullptr, nullptr, nullptr, (flags & GB_TRAIN_REUSE) != 0,
              (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0,
-             exact ? 1 : max_groups, status};
+             exact ? 1 : max_groups, status, param};
   int grid = 1;
   if (!exact) {
     int rc = grid_for((const void *)var.pool, var.G, max_groups, max_src, &grid, s0_bytes(var, dim));
@@ -301,13 +324,14 @@ GB_API int gb_train_pool_list(float *Msrc, float *Mtgt, int dim, const int32_t *
   return launch_pool(var, a, grid, as_stream(stream_handle));
 }
 
-GB_API int gb_train_pool_balanced(float *Msrc, float *Mtgt, int dim, const int32_t *list,
-                                  const int64_t *first, const int32_t *cnt, const int32_t *npos,
-                                  const int64_t *count, int64_t max_src, int B, int64_t lo_t,
-                                  int64_t n_t, int n_neg, double lr, uint64_t seed,
-                                  uint64_t side, const int32_t *adj, int64_t lo_s,
-                                  uint64_t pool_side, unsigned flags, int64_t max_groups,
-                                  int64_t *status, void *stream_handle) {
+static int train_pool_balanced_impl(float *Msrc, float *Mtgt, int dim, const int32_t *list,
+                                    const int64_t *first, const int32_t *cnt, const int32_t *npos,
+                                    const int64_t *count, int64_t max_src, int B, int64_t lo_t,
+                                    int64_t n_t, int n_neg, double lr, uint64_t seed,
+                                    uint64_t side, const int32_t *adj, int64_t lo_s,
+                                    uint64_t pool_side, unsigned flags, int64_t max_groups,
+                                    int64_t *status, const PairParam *param,
+                                    void *stream_handle) {
   GB_REQUIRE(dim >= 1 && B >= 1 && n_neg >= 0 && max_src >= 0 && n_t >= 0,
              "gb_train_pool_balanced: bad sizes");
   GB_REQUIRE(Msrc && Mtgt && status && list && first && cnt && npos && count && adj,
@@ -321,13 +345,60 @@ GB_API int gb_train_pool_balanced(float *Msrc, float *Mtgt, int dim, const int32
   PoolArgs a{Msrc, Mtgt, dim, nullptr, max_src, B, lo_t, n_t, n_neg, lr, seed, side, nullptr,
              adj, lo_s, pool_side, list, count, first, cnt, npos,
              (flags & GB_TRAIN_REUSE) != 0, (flags & GB_TRAIN_FAST_SIGMOID) != 0,
-             !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status};
+             !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status, param};
   int grid = 1;
   if (!exact) {
     int rc = grid_for((const void *)var.pool, var.G, max_groups, max_src, &grid, s0_bytes(var, dim));
     if (rc) return rc;
   }
   return launch_pool(var, a, grid, as_stream(stream_handle));
+}
+
+GB_API int gb_train_pool_list(float *Msrc, float *Mtgt, int dim, const int32_t *list,
+                              const int32_t *targets, const int64_t *count, int64_t max_src,
+                              int B, int64_t lo_t, int64_t n_t, int n_neg, double lr,
+                              uint64_t seed, uint64_t side, unsigned flags, int64_t max_groups,
+                              int64_t *status, void *stream_handle) {
+  return train_pool_list_impl(Msrc, Mtgt, dim, list, targets, count, max_src, B, lo_t, n_t,
+                              n_neg, lr, seed, side, flags, max_groups, status, nullptr,
+                              stream_handle);
+}
+
+GB_API int gb_train_pool_list_dp(float *Msrc, float *Mtgt, int dim, const int32_t *list,
+                                 const int32_t *targets, const int64_t *count, int64_t max_src,
+                                 int B, int64_t lo_t, int64_t n_t, int n_neg, const void *param,
+                                 uint64_t side, unsigned flags, int64_t max_groups,
+                                 int64_t *status, void *stream_handle) {
+  GB_REQUIRE(param, "gb_train_pool_list_dp: null param");
+  return train_pool_list_impl(Msrc, Mtgt, dim, list, targets, count, max_src, B, lo_t, n_t,
+                              n_neg, 0.0, 0, side, flags, max_groups, status,
+                              static_cast<const PairParam *>(param), stream_handle);
+}
+
+GB_API int gb_train_pool_balanced(float *Msrc, float *Mtgt, int dim, const int32_t *list,
+                                  const int64_t *first, const int32_t *cnt, const int32_t *npos,
+                                  const int64_t *count, int64_t max_src, int B, int64_t lo_t,
+                                  int64_t n_t, int n_neg, double lr, uint64_t seed,
+                                  uint64_t side, const int32_t *adj, int64_t lo_s,
+                                  uint64_t pool_side, unsigned flags, int64_t max_groups,
+                                  int64_t *status, void *stream_handle) {
+  return train_pool_balanced_impl(Msrc, Mtgt, dim, list, first, cnt, npos, count, max_src, B,
+                                  lo_t, n_t, n_neg, lr, seed, side, adj, lo_s, pool_side, flags,
+                                  max_groups, status, nullptr, stream_handle);
+}
+
+GB_API int gb_train_pool_balanced_dp(float *Msrc, float *Mtgt, int dim, const int32_t *list,
+                                     const int64_t *first, const int32_t *cnt,
+                                     const int32_t *npos, const int64_t *count, int64_t max_src,
+                                     int B, int64_t lo_t, int64_t n_t, int n_neg,
+                                     const void *param, uint64_t side, const int32_t *adj,
+                                     int64_t lo_s, uint64_t pool_side, unsigned flags,
+                                     int64_t max_groups, int64_t *status, void *stream_handle) {
+  GB_REQUIRE(param, "gb_train_pool_balanced_dp: null param");
+  return train_pool_balanced_impl(Msrc, Mtgt, dim, list, first, cnt, npos, count, max_src, B,
+                                  lo_t, n_t, n_neg, 0.0, 0, side, adj, lo_s, pool_side, flags,
+                                  max_groups, status, static_cast<const PairParam *>(param),
+                                  stream_handle);
 }
 
 GB_API int gb_nonfinite_scan(const float *M, int64_t count, int64_t epoch, int64_t *status,
@@ -371,7 +442,9 @@ namespace {
 // _fill_pool_side (bigtrain.py:164-196): one thread per source vertex.
 __global__ void fill_pool_kernel(const int64_t *__restrict__ xadj, const int32_t *__restrict__ adj,
                                  int64_t lo_s, int64_t hi_s, int64_t lo_t, int64_t hi_t, int B,
-                                 uint64_t seed, uint64_t side, int32_t *__restrict__ out) {
+                                 uint64_t seed, uint64_t side, int32_t *__restrict__ out,
+                                 const PairParam *__restrict__ param) {
+  if (param) seed = param->seed;
   for (int64_t v = lo_s + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < hi_s;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e1 = xadj[v + 1];
@@ -395,8 +468,10 @@ __global__ void fill_pool_compact_kernel(const int64_t *__restrict__ xadj,
                                          int64_t hi_s, int64_t lo_t, int64_t hi_t, int B,
                                          uint64_t seed, uint64_t side, int32_t *__restrict__ list,
                                          int32_t *__restrict__ targets,
-                                         unsigned long long *count) {
+                                         unsigned long long *count,
+                                         const PairParam *__restrict__ param) {
   const int lane = threadIdx.x & 31;
+  if (param) seed = param->seed;
   for (int64_t v0 = lo_s + (int64_t)blockIdx.x * blockDim.x; v0 < hi_s;
        v0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t v = v0 + threadIdx.x;
@@ -434,8 +509,10 @@ __global__ void fill_pool_balanced_kernel(const int64_t *__restrict__ xadj,
                                           int32_t *__restrict__ list, int64_t *__restrict__ first,
                                           int32_t *__restrict__ cnt_out,
                                           int32_t *__restrict__ npos_out,
-                                          unsigned long long *count) {
+                                          unsigned long long *count,
+                                          const PairParam *__restrict__ param) {
   const int lane = threadIdx.x & 31;
+  if (param) seed = param->seed;
   for (int64_t v0 = lo_s + (int64_t)blockIdx.x * blockDim.x; v0 < hi_s;
        v0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t v = v0 + threadIdx.x;
@@ -468,11 +545,11 @@ __global__ void fill_pool_balanced_kernel(const int64_t *__restrict__ xadj,
 }  // namespace tk
 }  // namespace gb
 
-GB_API int gb_fill_pool_balanced(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
-                                 int64_t hi_s, int64_t lo_t, int64_t hi_t, int64_t BK,
-                                 uint64_t seed, uint64_t side, int32_t *list, int64_t *first,
-                                 int32_t *cnt, int32_t *npos, int64_t *count,
-                                 void *stream_handle) {
+static int fill_pool_balanced_impl(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
+                                   int64_t hi_s, int64_t lo_t, int64_t hi_t, int64_t BK,
+                                   uint64_t seed, uint64_t side, int32_t *list, int64_t *first,
+                                   int32_t *cnt, int32_t *npos, int64_t *count,
+                                   const PairParam *param, void *stream_handle) {
   GB_REQUIRE(xadj && adj && list && first && cnt && npos && count && BK >= 1 &&
                  hi_s >= lo_s && hi_t >= lo_t,
              "gb_fill_pool_balanced: bad args");
@@ -482,15 +559,15 @@ GB_API int gb_fill_pool_balanced(const int64_t *xadj, const int32_t *adj, int64_
   const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
   gb::tk::fill_pool_balanced_kernel<<<(int)blocks, 256, 0, as_stream(stream_handle)>>>(
       xadj, adj, lo_s, hi_s, lo_t, hi_t, BK, seed, side, list, first, cnt, npos,
-      reinterpret_cast<unsigned long long *>(count));
+      reinterpret_cast<unsigned long long *>(count), param);
   GB_CHECK_LAUNCH();
   return GB_OK;
 }
 
-GB_API int gb_fill_pool_compact(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
-                                int64_t hi_s, int64_t lo_t, int64_t hi_t, int B, uint64_t seed,
-                                uint64_t side, int32_t *list, int32_t *targets, int64_t *count,
-                                void *stream_handle) {
+static int fill_pool_compact_impl(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
+                                  int64_t hi_s, int64_t lo_t, int64_t hi_t, int B, uint64_t seed,
+                                  uint64_t side, int32_t *list, int32_t *targets, int64_t *count,
+                                  const PairParam *param, void *stream_handle) {
   GB_REQUIRE(xadj && adj && list && targets && count && B >= 1 && hi_s >= lo_s && hi_t >= lo_t,
              "gb_fill_pool_compact: bad args");
   GB_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int64_t), as_stream(stream_handle)));
@@ -499,7 +576,59 @@ GB_API int gb_fill_pool_compact(const int64_t *xadj, const int32_t *adj, int64_t
   const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
   gb::tk::fill_pool_compact_kernel<<<(int)blocks, 256, 0, as_stream(stream_handle)>>>(
       xadj, adj, lo_s, hi_s, lo_t, hi_t, B, seed, side, list, targets,
-      reinterpret_cast<unsigned long long *>(count));
+      reinterpret_cast<unsigned long long *>(count), param);
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
+GB_API int gb_fill_pool_balanced(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
+                                 int64_t hi_s, int64_t lo_t, int64_t hi_t, int64_t BK,
+                                 uint64_t seed, uint64_t side, int32_t *list, int64_t *first,
+                                 int32_t *cnt, int32_t *npos, int64_t *count,
+                                 void *stream_handle) {
+  return fill_pool_balanced_impl(xadj, adj, lo_s, hi_s, lo_t, hi_t, BK, seed, side, list, first,
+                                 cnt, npos, count, nullptr, stream_handle);
+}
+
+GB_API int gb_fill_pool_balanced_dp(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
+                                    int64_t hi_s, int64_t lo_t, int64_t hi_t, int64_t BK,
+                                    const void *param, uint64_t side, int32_t *list,
+                                    int64_t *first, int32_t *cnt, int32_t *npos, int64_t *count,
+                                    void *stream_handle) {
+  GB_REQUIRE(param, "gb_fill_pool_balanced_dp: null param");
+  return fill_pool_balanced_impl(xadj, adj, lo_s, hi_s, lo_t, hi_t, BK, 0, side, list, first,
+                                 cnt, npos, count, static_cast<const PairParam *>(param),
+                                 stream_handle);
+}
+
+GB_API int gb_fill_pool_compact(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
+                                int64_t hi_s, int64_t lo_t, int64_t hi_t, int B, uint64_t seed,
+                                uint64_t side, int32_t *list, int32_t *targets, int64_t *count,
+                                void *stream_handle) {
+  return fill_pool_compact_impl(xadj, adj, lo_s, hi_s, lo_t, hi_t, B, seed, side, list, targets,
+                                count, nullptr, stream_handle);
+}
+
+GB_API int gb_fill_pool_compact_dp(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
+                                   int64_t hi_s, int64_t lo_t, int64_t hi_t, int B,
+                                   const void *param, uint64_t side, int32_t *list,
+                                   int32_t *targets, int64_t *count, void *stream_handle) {
+  GB_REQUIRE(param, "gb_fill_pool_compact_dp: null param");
+  return fill_pool_compact_impl(xadj, adj, lo_s, hi_s, lo_t, hi_t, B, 0, side, list, targets,
+                                count, static_cast<const PairParam *>(param), stream_handle);
+}
+
+static int fill_pool_side_impl(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
+                               int64_t hi_s, int64_t lo_t, int64_t hi_t, int B, uint64_t seed,
+                               uint64_t side, int32_t *out, const PairParam *param,
+                               void *stream_handle) {
+  GB_REQUIRE(xadj && out && B >= 1 && hi_s >= lo_s && hi_t >= lo_t,
+             "gb_fill_pool_side: bad args");
+  const int64_t n = hi_s - lo_s;
+  if (n == 0) return GB_OK;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+  gb::tk::fill_pool_kernel<<<(int)blocks, 256, 0, as_stream(stream_handle)>>>(
+      xadj, adj, lo_s, hi_s, lo_t, hi_t, B, seed, side, out, param);
   GB_CHECK_LAUNCH();
   return GB_OK;
 }
@@ -507,13 +636,15 @@ GB_API int gb_fill_pool_compact(const int64_t *xadj, const int32_t *adj, int64_t
 GB_API int gb_fill_pool_side(const int64_t *xadj, const int32_t *adj, int64_t lo_s, int64_t hi_s,
                              int64_t lo_t, int64_t hi_t, int B, uint64_t seed, uint64_t side,
                              int32_t *out, void *stream_handle) {
-  GB_REQUIRE(xadj && out && B >= 1 && hi_s >= lo_s && hi_t >= lo_t,
-             "gb_fill_pool_side: bad args");
-  const int64_t n = hi_s - lo_s;
-  if (n == 0) return GB_OK;
-  const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
-  gb::tk::fill_pool_kernel<<<(int)blocks, 256, 0, as_stream(stream_handle)>>>(
-      xadj, adj, lo_s, hi_s, lo_t, hi_t, B, seed, side, out);
-  GB_CHECK_LAUNCH();
-  return GB_OK;
+  return fill_pool_side_impl(xadj, adj, lo_s, hi_s, lo_t, hi_t, B, seed, side, out, nullptr,
+                             stream_handle);
+}
+
+GB_API int gb_fill_pool_side_dp(const int64_t *xadj, const int32_t *adj, int64_t lo_s,
+                                int64_t hi_s, int64_t lo_t, int64_t hi_t, int B,
+                                const void *param, uint64_t side, int32_t *out,
+                                void *stream_handle) {
+  GB_REQUIRE(param, "gb_fill_pool_side_dp: null param");
+  return fill_pool_side_impl(xadj, adj, lo_s, hi_s, lo_t, hi_t, B, 0, side, out,
+                             static_cast<const PairParam *>(param), stream_handle);
 }

@@ -982,6 +982,11 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 
 // Pool side (bigtrain.py:215-238), optionally drawing the pool on the fly
 // (bigtrain.py:164-196) from the device CSR.
 // ---------------------------------------------------------------------------
+struct PairParam {
+  uint64_t seed;
+  double lr;
+};
+
 struct PoolArgs {
   float *Msrc;
   float *Mtgt;
@@ -1014,6 +1019,10 @@ struct PoolArgs {
   bool atomic;
   int64_t max_groups;
   int64_t *status;
+  // device-resident {seed, lr} overriding the two arguments above when set
+  // (*_dp entry points: a captured rotation's launches read this rotation's
+  // values from a table the host rewrites before each graph replay)
+  const PairParam *__restrict__ param;
 };
 
 // lower_bound over adj[lo, hi) (rows are sorted ascending).
@@ -1067,6 +1076,8 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
   const int total = a.B * per_t;
   const int gbase = (int)(threadIdx.x & 31) - g.gl;
   const int64_t n = a.src_list ? min(a.n_src, *a.n_list) : a.n_src;
+  const uint64_t seed = a.param ? a.param->seed : a.seed;
+  const double lr = a.param ? a.param->lr : a.lr;
   bool bad = false;
   unsigned long long pos_count = 0, neg_count = 0;
 
@@ -1087,7 +1098,7 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
       first = __ldg(a.bal_first + k);
       cnt = __ldg(a.bal_cnt + k);
       npos = __ldg(a.bal_npos + k);
-      pkey = stream_key(a.seed, a.pool_side, 0, (uint64_t)(a.lo_s + i));
+      pkey = stream_key(seed, a.pool_side, 0, (uint64_t)(a.lo_s + i));
       tot = total + max(0, npos - a.B);
     } else if (!HOT && trow == nullptr) {
       const int64_t v = a.lo_s + i;
@@ -1095,9 +1106,9 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
       first = lower_bound_adj(a.adj, e0, e1, a.lo_t);
       cnt = lower_bound_adj(a.adj, first, e1, a.lo_t + a.n_t) - first;
       if (cnt == 0) continue;  // every slot is -1
-      pkey = stream_key(a.seed, a.pool_side, 0, (uint64_t)v);
+      pkey = stream_key(seed, a.pool_side, 0, (uint64_t)v);
     }
-    const uint64_t key = stream_key(a.seed, a.side, 1, (uint64_t)i);
+    const uint64_t key = stream_key(seed, a.side, 1, (uint64_t)i);
     Row S;
     SrcKeep<Row, kS0Smem> keep(kS0Smem ? group_smem<Row>(a.dim) : nullptr);
     bool loaded = false;
@@ -1174,7 +1185,7 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
         pos_count += __popc(pos_mask);
         neg_count += (ids[0] >= 0) + (ids[1] >= 0) + (ids[2] >= 0) + (ids[3] >= 0) -
                      __popc(pos_mask);
-        run_chunk<Row, EXACT>(S, i, ids, pos_mask, a.Mtgt, a.dim, a.lr, reuse, diagonal, true, g,
+        run_chunk<Row, EXACT>(S, i, ids, pos_mask, a.Mtgt, a.dim, lr, reuse, diagonal, true, g,
                               bad, fast, atomic);
       }
     }

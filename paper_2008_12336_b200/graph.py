@@ -151,6 +151,8 @@ class Graph:
         if (steps < 0).any():
             raise ValueError("xadj must be nondecreasing")
         if self.num_edges:
+            if a.shape[0] != self.num_edges:  # truncated file: numpy's broadcast ValueError
+                raise ValueError(f"adj holds {a.shape[0]} entries, |E| = {self.num_edges}")
             if a.min() < 0 or a.max() >= self.num_vertices:
                 raise ValueError("adj entry out of range")
             # strictly ascending inside each row: a rise must occur at every
@@ -322,14 +324,12 @@ def densify(g: Graph) -> tuple[Graph, np.ndarray]:
     return Graph(k, E, directed=g.directed, xadj_dev=x2[:k + 1].clone(), adj_dev=a2), kept_h
 
 
-def load_edge_list(text_stream: IO[str], directed: bool = False) -> Graph:
-    """Edge-list text, one "u v" per line, '#' comments and blank lines
-    skipped; ids densified in ascending order with the originals kept in
-    orig_ids (graph.py:134-171).  Parsing is host work; the CSR is built on
-    the GPU."""
+def _parse_edge_lines_host(lines, line_base: int = 0):
+    """The reference's per-line loop (graph.py:143-157) over `lines`; returns
+    (us, vs) lists or raises EdgeListParseError with the global line number."""
     us: list[int] = []
     vs: list[int] = []
-    for lineno, raw in enumerate(text_stream, start=1):
+    for lineno, raw in enumerate(lines, start=line_base + 1):
         line = raw.strip()
         if not line or line[0] == "#":
             continue
@@ -342,15 +342,117 @@ def load_edge_list(text_stream: IO[str], directed: bool = False) -> Graph:
             raise EdgeListParseError(lineno, f"non-integer vertex id in {line!r}") from None
         us.append(u)
         vs.append(v)
-    if not us:
-        raise EmptyGraphError("edge list contains no edges")
-    u_arr = np.asarray(us, dtype=np.int64)
-    v_arr = np.asarray(vs, dtype=np.int64)
-    ids = np.unique(np.concatenate([u_arr, v_arr]))
-    src = torch.from_numpy(np.searchsorted(ids, u_arr).astype(np.int64))
-    dst = torch.from_numpy(np.searchsorted(ids, v_arr).astype(np.int64))
+    return us, vs
+
+
+def _edges_to_graph(src: torch.Tensor, dst: torch.Tensor, directed: bool) -> Graph:
+    """Densify ids in ascending order (graph.py:160-164) and build the CSR
+    (self-loops dropped, symmetrized unless directed) -- on the GPU."""
+    m = int(src.numel())
+    ids = torch.cat([src, dst])
+    uniq = torch.empty(2 * m, dtype=torch.int64, device="cuda")
+    ws, wsb = _lib.workspace("gb_unique_ids_workspace", 2 * m)
+    k = C.c_int64(0)
+    _lib.call("gb_unique_ids", _lib.ptr(ids), 2 * m, _lib.ptr(uniq), C.byref(k), 1,
+              _lib.ptr(ws), wsb, _lib.stream())
+    del ws
+    orig = uniq[: int(k.value)].cpu().numpy()
     flags = _lib.GB_CSR_DROP_SELF | (0 if directed else _lib.GB_CSR_SYMMETRIZE)
-    return _csr_device(int(ids.shape[0]), src, dst, flags, directed, orig_ids=ids)
+    return _csr_device(int(k.value), ids[:m], ids[m:], flags, directed, orig_ids=orig)
+
+
+EDGE_TEXT_CHUNK = 256 << 20  # characters per device parse
+
+
+def load_edge_list(text_stream: IO[str], directed: bool = False) -> Graph:
+    """Edge-list text, one "u v" per line, '#' comments and blank lines
+    skipped; ids densified in ascending order with the originals kept in
+    orig_ids (graph.py:134-171).
+
+    On a GPU the text is parsed on the device (gb_parse_edge_text: one thread
+    per line, Python int() syntax) chunk by chunk, and the ids are densified
+    there (gb_unique_ids) before the CSR build; errors are the reference's
+    (the first malformed line is re-read by the host loop for its message;
+    a valid id outside int64 raises OverflowError after the whole input, as
+    numpy's conversion does).  Non-ASCII chunks go through the host loop.
+    Without a GPU the host loop parses everything (the CSR still needs one)."""
+    if not torch.cuda.is_available():
+        us, vs = _parse_edge_lines_host(text_stream)
+        if not us:
+            raise EmptyGraphError("edge list contains no edges")
+        u_arr = np.asarray(us, dtype=np.int64)
+        v_arr = np.asarray(vs, dtype=np.int64)
+        return _edges_to_graph(torch.from_numpy(u_arr), torch.from_numpy(v_arr), directed)
+    _lib.require_cuda()
+    parts_u: list[torch.Tensor] = []
+    parts_v: list[torch.Tensor] = []
+    line_base, overflow, carry = 0, False, ""
+    ws = None
+    wsb = 0
+    while True:
+        s = text_stream.read(EDGE_TEXT_CHUNK)
+        eof = not s
+        buf = carry + s
+        if not eof:
+            cut = buf.rfind("\n")
+            if cut < 0:
+                carry = buf
+                continue
+            body, carry = buf[:cut + 1], buf[cut + 1:]
+        else:
+            body, carry = buf, ""
+        if body:
+            if not body.isascii():
+                lines = body.split("\n")
+                if body.endswith("\n"):
+                    lines.pop()
+                us, vs = _parse_edge_lines_host(lines, line_base)
+                if any(not -2**63 <= x < 2**63 for x in us + vs):
+                    overflow = True
+                elif us:
+                    parts_u.append(torch.tensor(us, dtype=torch.int64))
+                    parts_v.append(torch.tensor(vs, dtype=torch.int64))
+                line_base += len(lines)
+            else:
+                raw = body.encode("ascii")
+                n = len(raw)
+                text = torch.frombuffer(bytearray(raw), dtype=torch.uint8).cuda()
+                need = C.c_size_t(0)
+                _lib.call("gb_parse_edge_text_workspace", n, C.byref(need))
+                if ws is None or wsb < need.value:
+                    ws = None
+                    ws, wsb = _lib.workspace("gb_parse_edge_text_workspace", n)
+                cap = n // 2 + 1
+                du = torch.empty(cap, dtype=torch.int64, device="cuda")
+                dv = torch.empty(cap, dtype=torch.int64, device="cuda")
+                res = (C.c_int64 * 4)()
+                _lib.call("gb_parse_edge_text", _lib.ptr(text), n, _lib.ptr(du), _lib.ptr(dv),
+                          res, _lib.ptr(ws), wsb, _lib.stream())
+                m, L, bad, over = (int(x) for x in res)
+                if bad >= 0:
+                    lines = body.split("\n")
+                    _parse_edge_lines_host(lines[bad:bad + 1], line_base + bad)
+                    # the device flagged a line the host accepts: trust the host
+                    us, vs = _parse_edge_lines_host(
+                        lines[:-1] if body.endswith("\n") else lines, line_base)
+                    du = torch.tensor(us, dtype=torch.int64, device="cuda")
+                    dv = torch.tensor(vs, dtype=torch.int64, device="cuda")
+                    m = len(us)
+                overflow = overflow or bool(over)
+                parts_u.append(du[:m])
+                parts_v.append(dv[:m])
+                line_base += L
+        if eof:
+            break
+    ws = None
+    if overflow:
+        raise OverflowError("Python int too large to convert to C long")
+    m = sum(int(t.numel()) for t in parts_u)
+    if m == 0:
+        raise EmptyGraphError("edge list contains no edges")
+    src = torch.cat([t.cuda() for t in parts_u])
+    dst = torch.cat([t.cuda() for t in parts_v])
+    return _edges_to_graph(src, dst, directed)
 
 
 def write_edge_list(g: Graph, text_stream: IO[str]) -> None:
@@ -371,16 +473,51 @@ def degree(g: Graph, v: int) -> int:
 
 def save_graph(g: Graph, path: str) -> None:
     """GSHG binary cache: magic, u32 version, u64 V, u64 E, u64 xadj[V+1],
-    u32 adj[E], little-endian (graph.py:192-200)."""
+    u32 adj[E], little-endian (graph.py:192-200).  A device-resident graph is
+    streamed out through pinned chunks (no host copy of the CSR)."""
     header = GRAPH_MAGIC + struct.pack("<IQQ", GRAPH_VERSION, g.num_vertices, g.num_edges)
     with open(path, "wb") as f:
         f.write(header)
+        if g._xadj is None and g._xadj_dev is not None and torch.cuda.is_available():
+            from ._staging import device_to_file
+            x, a = g.device_csr()
+            device_to_file(f, x[: g.num_vertices + 1].contiguous().view(torch.uint8))
+            device_to_file(f, a[: g.num_edges].contiguous().view(torch.uint8))
+            return
         f.write(np.ascontiguousarray(g.xadj, dtype="<u8").tobytes())
         f.write(np.ascontiguousarray(g.adj, dtype="<u4").tobytes())
 
 
+_VALIDATE_MESSAGES = ((1, "xadj endpoints inconsistent with |E|"),
+                      (2, "xadj must be nondecreasing"),
+                      (4, "adj entry out of range"),
+                      (8, "adjacency rows must be strictly ascending"))
+
+
+def validate_device(g: Graph) -> None:
+    """Graph.validate (graph.py:61-77) on the device CSR: one coalesced pass
+    over xadj and adj (gb_csr_validate); the reference's messages, first
+    failing check first."""
+    x, a = g.device_csr()
+    if x.numel() != g.num_vertices + 1:
+        raise ValueError("xadj length must be |V|+1")
+    ws, wsb = _lib.workspace("gb_csr_validate_workspace", g.num_edges)
+    flags = C.c_int(0)
+    _lib.call("gb_csr_validate", g.num_vertices, g.num_edges, _lib.ptr(x),
+              _lib.ptr(a) if g.num_edges else None, C.byref(flags), _lib.ptr(ws), wsb,
+              _lib.stream())
+    for bit, msg in _VALIDATE_MESSAGES:
+        if flags.value & bit:
+            raise ValueError(msg)
+
+
 def load_graph(path: str, directed: bool = False) -> Graph:
-    """Read a GSHG file written by save_graph (graph.py:203-219)."""
+    """Read a GSHG file written by save_graph (graph.py:203-219).  On a GPU
+    the arrays are streamed straight into HBM through pinned chunks and
+    validated there (validate_device): the result is a device-backed Graph
+    whose host arrays materialise on first use.  Without a GPU, or for a
+    truncated file (so the reference's error is raised), the host path."""
+    import os
     with open(path, "rb") as f:
         magic = f.read(4)
         if magic != GRAPH_MAGIC:
@@ -389,6 +526,17 @@ def load_graph(path: str, directed: bool = False) -> Graph:
         if version != GRAPH_VERSION:
             raise ValueError(f"unsupported cache version {version}")
         nv, ne = struct.unpack("<QQ", f.read(16))
+        full = os.fstat(f.fileno()).st_size >= 24 + 8 * (nv + 1) + 4 * ne
+        if torch.cuda.is_available() and full and nv < 2**62:
+            from ._staging import file_to_device
+            _lib.require_cuda()
+            x = torch.empty(nv + 1, dtype=torch.int64, device="cuda")
+            a = torch.empty(max(ne, 1), dtype=torch.int32, device="cuda")
+            file_to_device(f, x.view(torch.uint8), 8 * (nv + 1))
+            file_to_device(f, a.view(torch.uint8), 4 * ne)
+            g = Graph(int(nv), int(ne), directed=directed, xadj_dev=x, adj_dev=a)
+            validate_device(g)
+            return g
         xadj = np.fromfile(f, dtype="<u8", count=nv + 1).astype(np.int64)
         adj = np.fromfile(f, dtype="<u4", count=ne).astype(np.int32)
     g = Graph(int(nv), int(ne), xadj=xadj, adj=adj, directed=directed)

@@ -139,6 +139,7 @@ class PairStep:
     hi_b: int
     seed: int
     lr: float
+    param: int | None = None  # device {seed, lr} (CUDA-graph rotations)
 
 
 PairFn = Callable[[torch.Tensor, torch.Tensor, PairStep], None]
@@ -163,17 +164,18 @@ class DevicePair:
     def prepare(self, s: PairStep, tag: str = "0") -> None:
         if s.hi_a - s.lo_a <= 0 or s.hi_b - s.lo_b <= 0:
             return
-        self.sides.prepare(s.lo_a, s.hi_a, s.lo_b, s.hi_b, s.seed, 0, tag + "a")
+        self.sides.prepare(s.lo_a, s.hi_a, s.lo_b, s.hi_b, s.seed, 0, tag + "a", s.param)
         if s.a != s.b:
-            self.sides.prepare(s.lo_b, s.hi_b, s.lo_a, s.hi_a, s.seed, 1, tag + "b")
+            self.sides.prepare(s.lo_b, s.hi_b, s.lo_a, s.hi_a, s.seed, 1, tag + "b", s.param)
 
     def train(self, Ma: torch.Tensor, Mb: torch.Tensor, s: PairStep, tag: str = "0") -> None:
         if s.hi_a - s.lo_a <= 0 or s.hi_b - s.lo_b <= 0:
             return
-        self.sides.train(Ma, Mb, s.lo_a, s.hi_a, s.lo_b, s.hi_b, s.seed, s.lr, 0, 2, tag + "a")
+        self.sides.train(Ma, Mb, s.lo_a, s.hi_a, s.lo_b, s.hi_b, s.seed, s.lr, 0, 2, tag + "a",
+                         s.param)
         if s.a != s.b:
             self.sides.train(Mb, Ma, s.lo_b, s.hi_b, s.lo_a, s.hi_a, s.seed, s.lr, 1, 3,
-                             tag + "b")
+                             tag + "b", s.param)
 
     def __call__(self, Ma: torch.Tensor, Mb: torch.Tensor, s: PairStep) -> None:
         self.prepare(s, "x")
@@ -545,9 +547,41 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
             fns = {r: device_pair_fn(g, cfg, B, K, status)[0] for r in store.local}
     has_prepare = on_gpu
 
+    # CUDA-graph rotations (one process holding every rank on the device):
+    # a rotation is the same launch sequence each time -- the circle shifts
+    # relabel parts and return to the initial arrangement after K-1 rounds --
+    # except for the pairs' seeds and lr, which the *_dp kernels read from a
+    # device table.  Rotation 0 runs eagerly (allocating every pool buffer),
+    # the next is captured once, and each later rotation is one table upload
+    # + one replay: the host's ~2 launches per pair side leave the path.
+    use_graph = (has_prepare and not distributed and not store.host and
+                 exchange_events is None and rotations >= 2 and
+                 first.sides.mode != "fused" and
+                 os.environ.get("GB_ROTATION_GRAPH", "1") != "0")
+    ptab = None
+    if use_graph:
+        ptab = torch.zeros((P, 2), dtype=torch.int64, device=store.device)
+        hbuf = [torch.zeros((P, 2), dtype=torch.int64).pin_memory() for _ in range(2)]
+        hev: list = [None, None]
+
+        def upload(rot):
+            k = rot % 2
+            if hev[k] is not None:
+                hev[k].synchronize()  # the previous copy out of this buffer is done
+            h = hbuf[k].numpy()
+            seeds = np.array([_lib.u64(_derived_seed(cfg.seed, rng_stream, rot * P + q))
+                              for q in range(P)], dtype=np.uint64)
+            h[:, 0] = seeds.view(np.int64)
+            h[:, 1] = np.full(P, lr_at(cfg.learning_rate, rot, rotations),
+                              dtype=np.float64).view(np.int64)
+            ptab.copy_(hbuf[k], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            hev[k] = ev
+
     sent_bytes, n_pairs = 0, 0
     t0 = time.perf_counter()
-    main = torch.cuda.current_stream(store.device) if store.device.type == "cuda" else None
+    main0 = torch.cuda.current_stream(store.device) if store.device.type == "cuda" else None
 
     def round_steps(rot, ri, arr):
         diagonal = ri == 0
@@ -559,8 +593,9 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
                 lo_a, hi_a = plan.part_range(a)
                 lo_b, hi_b = plan.part_range(b)
                 seed = _derived_seed(cfg.seed, rng_stream, rot * P + index[(a, b)])
+                prm = ptab.data_ptr() + 16 * index[(a, b)] if ptab is not None else None
                 lst.append((k, PairStep(a, b, lo_a, hi_a, lo_b, hi_b, seed,
-                                        lr_at(cfg.learning_rate, rot, rotations))))
+                                        lr_at(cfg.learning_rate, rot, rotations), prm)))
             out.append((r, lst))
         return out
 
@@ -580,11 +615,15 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
             ctx = torch.cuda.stream(streams[r]) if streams else _null()
             with ctx:
                 if streams:
-                    streams[r].wait_stream(main)
+                    streams[r].wait_stream(steps_fn_main)
                 for k, s in lst:
                     fns[r].prepare(s, tag(ri, r, k))
 
-    for rot in range(rotations):
+    def run_rotation(rot, main):
+        """All rounds of one rotation; returns (pairs, bytes shifted)."""
+        nonlocal steps_fn_main
+        steps_fn_main = main
+        pairs, sent = 0, 0
         arr = initial_arrangement(K)
         steps = round_steps(rot, 0, arr)
         prepare(steps, 0)
@@ -604,7 +643,7 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
                             fns[r].train(Ma, Mb, s, tag(ri, r, k))
                         else:
                             pair_fn(Ma, Mb, s)
-                        n_pairs += 1
+                        pairs += 1
                     store.end_pair(r)
             if streams:
                 for st_r in streams.values():
@@ -619,8 +658,8 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
                 if exchange_events is not None and main is not None:
                     e0 = torch.cuda.Event(enable_timing=True)
                     e0.record(main)
-                sent_bytes += store.shift(moves, arr, group, per_process=per_process,
-                                          before_wait=after if per_process else None)
+                sent += store.shift(moves, arr, group, per_process=per_process,
+                                    before_wait=after if per_process else None)
                 if exchange_events is not None and main is not None:
                     e1 = torch.cuda.Event(enable_timing=True)
                     e1.record(main)
@@ -631,6 +670,24 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
             elif nxt:
                 prepare(nxt, ri + 1)
             steps = nxt
+        return pairs, sent
+
+    steps_fn_main = main0
+    if use_graph:
+        upload(0)
+        pr, sb = run_rotation(0, main0)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, capture_error_mode="relaxed"):
+            run_rotation(1, torch.cuda.current_stream(store.device))
+        for rot in range(1, rotations):
+            upload(rot)
+            graph.replay()
+        n_pairs, sent_bytes = pr * rotations, sb * rotations
+    else:
+        for rot in range(rotations):
+            pr, sb = run_rotation(rot, main0)
+            n_pairs += pr
+            sent_bytes += sb
     store.drain()
     if store.device.type == "cuda":
         torch.cuda.current_stream(store.device).synchronize()

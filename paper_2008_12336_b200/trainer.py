@@ -387,14 +387,26 @@ def _host(M) -> np.ndarray:
 
 def save_embedding(M, path: str) -> None:
     """GSHE: magic, u32 version, u64 rows, u32 dim, f32 rows little-endian
-    (trainer.py:291-298)."""
+    (trainer.py:291-298).  A CUDA matrix is streamed out of HBM through
+    pinned chunks (no full host copy)."""
+    if isinstance(M, torch.Tensor) and M.is_cuda:
+        from ._staging import device_to_file
+        if M.dim() != 2 or M.dtype != torch.float32:
+            raise TypeError("embedding must be a 2-D float32 matrix")
+        with open(path, "wb") as f:
+            f.write(EMBED_MAGIC + struct.pack("<IQI", EMBED_VERSION, M.shape[0], M.shape[1]))
+            device_to_file(f, M.contiguous().view(-1).view(torch.uint8))
+        return
     A = np.ascontiguousarray(_host(M), dtype="<f4")
     with open(path, "wb") as f:
         f.write(EMBED_MAGIC + struct.pack("<IQI", EMBED_VERSION, A.shape[0], A.shape[1]))
         f.write(A.tobytes())
 
 
-def load_embedding(path: str) -> np.ndarray:
+def load_embedding(path: str, device: bool = False):
+    """Read a GSHE file (trainer.py:301-312) as a numpy float32 matrix; with
+    device=True straight into a CUDA tensor through pinned chunks."""
+    import os
     with open(path, "rb") as f:
         magic = f.read(4)
         if magic != EMBED_MAGIC:
@@ -403,8 +415,15 @@ def load_embedding(path: str) -> np.ndarray:
         if version != EMBED_VERSION:
             raise ValueError(f"unsupported embedding version {version}")
         rows, dim = struct.unpack("<QI", f.read(12))
+        if device and os.fstat(f.fileno()).st_size >= 20 + 4 * rows * dim:
+            from ._staging import file_to_device
+            _lib.require_cuda()
+            out = torch.empty((rows, dim), dtype=torch.float32, device="cuda")
+            file_to_device(f, out.view(-1).view(torch.uint8), 4 * rows * dim)
+            return out
         data = np.fromfile(f, dtype="<f4", count=rows * dim)
-    return data.reshape(rows, dim).astype(np.float32)
+    A = data.reshape(rows, dim).astype(np.float32)
+    return torch.from_numpy(A).cuda() if device else A
 
 
 def write_embedding_tsv(M, stream: IO[str], orig_ids: np.ndarray | None = None) -> None:

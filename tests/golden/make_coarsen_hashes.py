@@ -9,7 +9,8 @@ its deterministic ladder) on that CSR and records, per level, the vertex and
 arc counts and position-keyed checksums (oracle.checksum == device
 gb_checksum) of xadj, adj and the level's map -- the arrays are GBs, so the
 fixture holds their checksums.  The oracle's own coarsen_all is run beside it
-as a cross-check.  Writes tests/golden/coarsen_c3_hashes.json.
+as a cross-check.  Writes tests/golden/coarsen_<name>_hashes.json (c3; and
+"s24": scale 24, 400M samples -- 9.7M vertices, 769M arcs, 6 levels).
 """
 import json
 import os
@@ -24,7 +25,11 @@ os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
 import mlembed as ml  # noqa: E402
 from oracle import oracle as orc  # noqa: E402
 
+# python make_coarsen_hashes.py [scale samples name]   (default: the C3 shape)
 SCALE, SAMPLES, SEED = 22, 126_000_000, 7
+NAME = "c3"
+if len(sys.argv) > 3:
+    SCALE, SAMPLES, NAME = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
 
 
 def level_hashes(graphs, maps):
@@ -62,6 +67,6 @@ out = {"graph": {"scale": SCALE, "samples": SAMPLES, "seed": SEED, "densified": 
        "checksum": "sum_i mix64((i * 0x9E3779B97F4A7C15) ^ int64(x[i])) mod 2^64",
        "source": "reference mlembed.coarsen_all(num_workers=1); oracle coarsen_all identical",
        "seconds": {"generate": t_gen, "reference_coarsen": t_ref, "oracle_coarsen": t_orc}}
-with open(os.path.join(ROOT, "tests", "golden", "coarsen_c3_hashes.json"), "w") as f:
+with open(os.path.join(ROOT, "tests", "golden", f"coarsen_{NAME}_hashes.json"), "w") as f:
     json.dump(out, f, indent=1)
 print(json.dumps(out["seconds"]))

@@ -346,9 +346,87 @@ def make_eval():
     save("eval.npz", **out)
 
 
+def _edge_text(rng, n_lines, id_pool, bad_at=None):
+    """Edge-list text exercising the parser: comments (leading whitespace
+    too), blank and whitespace-only lines, tabs / CR / vertical tab
+    separators, signs, leading zeros, digit underscores, negative and sparse
+    ids, duplicates and self-loops."""
+    out = []
+    for i in range(n_lines):
+        r = rng.random()
+        if r < 0.04:
+            out.append("# comment %d" % i)
+        elif r < 0.06:
+            out.append("   #indented comment")
+        elif r < 0.08:
+            out.append(" \t ")
+        else:
+            u, v = (int(x) for x in rng.choice(id_pool, size=2))
+            if rng.random() < 0.05:
+                v = u
+            fu, fv = str(u), str(v)
+            k = rng.random()
+            if k < 0.05 and u >= 0:
+                fu = "+" + fu
+            elif k < 0.1 and u >= 0:
+                fu = "00" + fu
+            elif k < 0.15 and len(fv) > 2 and v >= 0:
+                fv = fv[0] + "_" + fv[1:]
+            sep = [" ", "\t", "  ", " \x0b"][int(rng.integers(4))]
+            tail = ["", " ", "\r", "\t"][int(rng.integers(4))]
+            out.append(fu + sep + fv + tail)
+    if bad_at is not None:
+        out[bad_at[0]] = bad_at[1]
+    return "\n".join(out) + "\n"
+
+
+def make_edgelist():
+    """load_edge_list (graph.py:134-171): parsed CSR + orig_ids of texts, and
+    the exact error (type, line, message) of malformed ones."""
+    import io
+    from mlembed import errors as rerr
+    rng = np.random.default_rng(21)
+    out = {}
+    pools = [np.arange(0, 50), np.concatenate([-np.arange(1, 30), 10**np.arange(3, 18)]),
+             rng.integers(-2**62, 2**62, size=300)]
+    k = 0
+    for pool in pools:
+        for directed in (False, True):
+            t = _edge_text(rng, 400, pool)
+            g = ml.load_edge_list(io.StringIO(t), directed=directed)
+            out[f"t{k}_text"] = np.frombuffer(t.encode("ascii"), dtype=np.uint8)
+            out[f"t{k}_directed"] = np.int64(directed)
+            out[f"t{k}_xadj"] = g.xadj
+            out[f"t{k}_adj"] = g.adj
+            out[f"t{k}_orig"] = g.orig_ids
+            k += 1
+    out["n_text"] = np.int64(k)
+    bad = ["1 2 3", "7", "x 4", "1_ 2", "1__2 3", "_1 2", "+-1 2", "0x10 3", "1.0 2",
+           "5 9 # trailing comment", "\u00e91 2", "99999999999999999999 1"]
+    e = 0
+    for b in bad:
+        for where in (3, 150):
+            t = _edge_text(rng, 200, pools[0], bad_at=(where, b))
+            try:
+                ml.load_edge_list(io.StringIO(t))
+                kind, line, msg = "none", 0, ""
+            except rerr.EdgeListParseError as ex:
+                kind, line, msg = "parse", ex.line_number, str(ex)
+            except OverflowError as ex:
+                kind, line, msg = "overflow", 0, str(ex)
+            out[f"e{e}_text"] = np.frombuffer(t.encode("utf-8"), dtype=np.uint8)
+            out[f"e{e}_kind"] = np.frombuffer(kind.encode(), dtype=np.uint8)
+            out[f"e{e}_line"] = np.int64(line)
+            out[f"e{e}_msg"] = np.frombuffer(msg.encode("utf-8"), dtype=np.uint8)
+            e += 1
+    out["n_err"] = np.int64(e)
+    save("edgelist.npz", **out)
+
+
 GENERATORS = {"rng": make_rng, "update": make_update, "train_pass": make_train_pass,
               "coarsen": make_coarsen, "csr": make_csr, "pool": make_pool,
-              "large": make_large_and_multilevel, "rmat": make_rmat, "eval": make_eval}
+              "large": make_large_and_multilevel, "rmat": make_rmat, "eval": make_eval,
+              "edgelist": make_edgelist}
 
 if __name__ == "__main__":
     for name in (sys.argv[1:] or GENERATORS):

@@ -192,6 +192,48 @@ def test_device_tournament_deterministic_bit_exact(cuda, orc, G):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("G", [1, 2, 4])
+def test_rotation_graph_deterministic_bit_exact(cuda, orc, G, monkeypatch):
+    """Rotations 1.. replayed from one captured CUDA graph (seeds and lr from
+    the device table, *_dp kernels) equal the sequential replay bit for bit,
+    with the virtual ranks on their own streams (G > 1) and serialised."""
+    g, x, a = _graph(orc, scale=10, samples=6000)
+    cfg = gb.TrainConfig(dim=32, negative_samples=3, seed=4, deterministic=True)
+    M0 = orc.init_embedding(g.num_vertices, 32, 2)
+    ref = M0.copy()
+    rot = _sequential_replay(orc, g, x, a, ref, cfg, 60, G)
+    assert rot >= 2
+    for vs in ("1", "0"):
+        monkeypatch.setenv("GB_VIRTUAL_STREAMS", vs)
+        M = torch.from_numpy(M0.copy()).cuda()
+        st = tn.train_tournament(g, M, cfg, 60, num_ranks=G)
+        assert st["rotations"] == rot and st["pairs"] == rot * (2 * G) * (2 * G + 1) // 2
+        assert np.array_equal(M.cpu().numpy(), ref), vs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("balanced", [False, True])
+def test_rotation_graph_hogwild_matches_eager(cuda, orc, monkeypatch, balanced):
+    """Default (Hogwild) pools: the graph-replayed rotations draw exactly the
+    eager path's samples (equal positive/negative counts) and train to the
+    same matrix up to Hogwild interleaving."""
+    g, x, a = _graph(orc, scale=12, samples=40000)
+    cfg = gb.TrainConfig(dim=64, negative_samples=3, seed=4, balanced_pools=balanced)
+    M0 = torch.from_numpy(orc.init_embedding(g.num_vertices, 64, 2)).cuda()
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("GB_ROTATION_GRAPH", mode)
+        M = M0.clone()
+        st = tn.train_tournament(g, M, cfg, 200, num_ranks=4)
+        assert st["rotations"] >= 3
+        out[mode] = (M, st["pos_updates"], st["neg_updates"])
+    (Mg, pg, ng), (Me, pe, ne) = out["1"], out["0"]
+    assert (pg, ng) == (pe, ne) and pg > 0
+    rel = float((Mg - Me).norm() / (Me - M0).norm())
+    assert rel < 0.1, rel
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("G", [2, 3])
 def test_host_staged_parts_deterministic_bit_exact(cuda, orc, G):
     """Parts in pinned host memory staged through four device slots (the
