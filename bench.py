@@ -697,12 +697,12 @@ def run_tournament(args):
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32 rows / f64 dot",
         "data": "synthetic R-MAT generated on device (seeded, Graph500 parameters)",
-        "config": workload_config({
+        "config": ({
             "workload": f"part-pair tournament on the C2 graph, K={K} parts, B={B}, d={dim}",
             "dim": dim,
             "step": f"{R} rotations: each K(K+1)/2 pairs, K-1 part exchanges "
                     "(one process: rotation 0 eager, the rest replayed from a CUDA graph)",
-            "rotation_graph": os.environ.get("GB_ROTATION_GRAPH", "1") != "0",
+            "rotation_graph": os.environ.get("GB_ROTATION_GRAPH", "auto"),
             "parallelism": f"tournament over {world} GPU(s)"
                            + (f" ({vr} virtual ranks)" if world == 1 and vr > 1 else ""),
             "vertices": V, "pool_mode": os.environ.get("GB_POOL_MODE", "compact")}),
@@ -736,7 +736,7 @@ def main():
                          "strong scaling)")
     ap.add_argument("--dim", type=int, default=0,
                     help="tournament workload: embedding dimension (default 128; C5 uses 256)")
-    ap.add_argument("--rotations", type=int, default=8,
+    ap.add_argument("--rotations", type=int, default=32,
                     help="tournament workload: rotations per step")
     ap.add_argument("--virtual-ranks", type=int, default=1,
                     help="tournament on one GPU: run the schedule of R ranks (K = 2R parts) "

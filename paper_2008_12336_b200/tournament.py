@@ -554,10 +554,15 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
     # device table.  Rotation 0 runs eagerly (allocating every pool buffer),
     # the next is captured once, and each later rotation is one table upload
     # + one replay: the host's ~2 launches per pair side leave the path.
+    # GB_ROTATION_GRAPH: auto (>= 16 rotations: capture + instantiate cost
+    # ~2 eager rotations, a replay saves ~12% of one at K=16 on the C2 graph,
+    # profiles/r02_rotation_graph_phases.jsonl), 1 (from 2 rotations), 0 (off)
+    rg = os.environ.get("GB_ROTATION_GRAPH", "auto")
+    if rg not in ("auto", "0", "1"):
+        raise ConfigError(f"GB_ROTATION_GRAPH={rg!r}: expected auto, 0 or 1")
     use_graph = (has_prepare and not distributed and not store.host and
-                 exchange_events is None and rotations >= 2 and
-                 first.sides.mode != "fused" and
-                 os.environ.get("GB_ROTATION_GRAPH", "1") != "0")
+                 exchange_events is None and first.sides.mode != "fused" and
+                 rotations >= (2 if rg == "1" else 16) and rg != "0")
     ptab = None
     if use_graph:
         ptab = torch.zeros((P, 2), dtype=torch.int64, device=store.device)
@@ -673,15 +678,42 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
         return pairs, sent
 
     steps_fn_main = main0
+    trace = os.environ.get("GB_TRACE_ROTATIONS") == "1"
+    phases: dict[str, float] = {}
+
+    def mark(name, t_prev):
+        if trace:
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            phases[name] = phases.get(name, 0.0) + t - t_prev
+            return t
+        return t_prev
+
     if use_graph:
+        tp = time.perf_counter()
         upload(0)
         pr, sb = run_rotation(0, main0)
+        tp = mark("eager_rotation", tp)
+        # capture on a side stream with the bare capture API: torch.cuda.graph()
+        # would also gc.collect() and empty the caching allocator on entry,
+        # which costs more than the launches the graph saves
         graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, capture_error_mode="relaxed"):
-            run_rotation(1, torch.cuda.current_stream(store.device))
+        cap = torch.cuda.Stream(store.device)
+        cap.wait_stream(main0)
+        with torch.cuda.stream(cap):
+            graph.capture_begin(capture_error_mode="relaxed")
+            try:
+                run_rotation(1, cap)
+            finally:
+                graph.capture_end()
+        main0.wait_stream(cap)
+        tp = mark("capture", tp)
         for rot in range(1, rotations):
             upload(rot)
             graph.replay()
+        tp = mark("replays", tp)
+        del graph
+        mark("graph_destroy", tp)
         n_pairs, sent_bytes = pr * rotations, sb * rotations
     else:
         for rot in range(rotations):
@@ -718,6 +750,7 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
         "exchange_bytes": sent_bytes,
         "train_s": train_s,
         "part_device_bytes": store.device_bytes,
+        **({"phases_s": phases} if phases else {}),
     }
 
 

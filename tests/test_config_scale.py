@@ -5,7 +5,8 @@
   coarsen_all(num_workers=1) level by level: vertex/arc/cluster counts and
   position-keyed checksums of xadj, adj and map (tests/golden/
   coarsen_c3_hashes.json, made by make_coarsen_hashes.py from mlembed; the
-  oracle's hierarchy is identical).  The device computes the checksums
+  oracle's hierarchy is identical), and the same for an R-MAT scale-24
+  graph (9.7M vertices, 769M arcs; coarsen_s24_hashes.json).  The device computes the checksums
   (gb_checksum), so no GB-sized array leaves HBM.
 
 * Link-prediction AUCROC on C1 (the north star's third bar: within 0.01 of
@@ -33,8 +34,11 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 AUC_TOL = 0.01
 
 
-def test_c3_coarsening_matches_reference_checksums(cuda):
-    with open(os.path.join(GOLDEN, "coarsen_c3_hashes.json")) as f:
+@pytest.mark.parametrize("shape", ["c3", "s24"])
+def test_coarsening_matches_reference_checksums(cuda, shape):
+    """c3: the C3 shape; s24: R-MAT scale 24, 400M samples (9.7M vertices,
+    769M arcs, 6 levels) -- both from the reference's coarsen_all."""
+    with open(os.path.join(GOLDEN, f"coarsen_{shape}_hashes.json")) as f:
         gold = json.load(f)
     gg = gold["graph"]
     g = gb.rmat_graph(gg["scale"], gg["samples"], gg["seed"], densify_ids=True)

@@ -203,6 +203,7 @@ def test_rotation_graph_deterministic_bit_exact(cuda, orc, G, monkeypatch):
     ref = M0.copy()
     rot = _sequential_replay(orc, g, x, a, ref, cfg, 60, G)
     assert rot >= 2
+    monkeypatch.setenv("GB_ROTATION_GRAPH", "1")  # from 2 rotations (auto: 16)
     for vs in ("1", "0"):
         monkeypatch.setenv("GB_VIRTUAL_STREAMS", vs)
         M = torch.from_numpy(M0.copy()).cuda()
