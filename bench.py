@@ -255,20 +255,28 @@ def run_ours(args):
         raise FloatingPointError("non-finite embedding during the benchmark")
 
     # e2e through the public API with host buffers: one train_level call per
-    # step (one edge-scaled epoch = ceil(E/V) passes), M copied in from pinned
-    # host memory and back every step.
+    # step (one edge-scaled epoch = ceil(E/V) passes) on a host Graph (its CSR
+    # is uploaded and its source list built inside the step), M copied in
+    # from pinned host memory and back every step.
     M_host = torch.from_numpy(gb.init_embedding(V, DIM, 1)).pin_memory()
     cfg = gb.TrainConfig(dim=DIM, negative_samples=NNEG, seed=1, learning_rate=LR,
                          epoch_unit="edge-scaled", atomic_rows=(not args.store_rows))
     e2e_steps = max(2, min(args.steps // 10, 5))
-    gb.train_level(G, M_host, cfg, 1)  # warm-up
+    xh = torch.from_numpy(G.xadj).pin_memory().numpy()
+    ah = torch.from_numpy(np.ascontiguousarray(G.adj)).pin_memory().numpy()
+    csr_bytes = int(xh.nbytes + ah.nbytes)
+
+    def host_graph():
+        return gb.Graph(V, G.num_edges, xadj=xh, adj=ah)
+
+    gb.train_level(host_graph(), M_host, cfg, 1)  # warm-up
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     te = time.perf_counter()
     e2e_upd = 0
     for _ in range(e2e_steps):
-        st = gb.train_level(G, M_host, cfg, 1)
+        st = gb.train_level(host_graph(), M_host, cfg, 1)
         e2e_upd += st.updates
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - te
@@ -325,9 +333,9 @@ def run_ours(args):
                      "dram_frac": (traffic / (kern_ms / 1000.0) / 1e9 / peak
                                    if traffic else None)},
         "e2e": {"value": e2e_value, "unit": UNIT,
-                "h2d_bytes_per_step": V * DIM * 4, "d2h_bytes_per_step": V * DIM * 4,
-                "step": f"train_level(g, M_pinned_host, edge-scaled, e_i=1): {ppe} passes + "
-                        f"M in/out", "steps": e2e_steps},
+                "h2d_bytes_per_step": V * DIM * 4 + csr_bytes, "d2h_bytes_per_step": V * DIM * 4,
+                "step": f"train_level(host Graph, M_pinned_host, edge-scaled, e_i=1): CSR "
+                        f"upload + source list, {ppe} passes, M in/out", "steps": e2e_steps},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
         "fp64_sigmoid": {"value": upd_per_step / (ms64 / 1000.0), "unit": UNIT,
@@ -501,10 +509,12 @@ def sharded_c3(args, rank, world, print_line=True):
     upd = sent = 0
     with ClockSampler(torch.cuda.current_device()) as clk:
         t0.record(stream)
+        launches = 0
         for _ in range(args.steps):
             st = step(events)
             upd += st["pos_updates"] + st["neg_updates"]
             sent += st["exchange_bytes"]
+            launches += st["kernel_launches"]
         t1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -530,7 +540,7 @@ def sharded_c3(args, rank, world, print_line=True):
                         "nvlink_gbs_if_exposed": (sent / world / (exch_ms / 1000.0) / 1e9
                                                   if exch_ms > 0 and sent else None)},
            "part_bytes_per_gpu": store.device_bytes, "matrix_bytes": V * C3_DIM * 4,
-           "clocks": clk.summary()}
+           "gpu_launches": launches, "clocks": clk.summary()}
     del store
     return out, g
 
@@ -584,7 +594,7 @@ def run_sharded(args):
                 "d2h_bytes_per_step": g.num_vertices * C3_DIM * 4,
                 "step": "train_tournament(g, M pinned host): 2 parts in, trained, all_gather "
                         "back to every rank's host matrix", "steps": e2e_steps},
-        "gpu_launches": None, "clocks": res["clocks"],
+        "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -676,10 +686,11 @@ def run_tournament(args):
     t1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
         t0.record(stream)
-        upd = 0
+        upd = launches = 0
         for _ in range(args.steps):
             st = step()
             upd += st["pos_updates"] + st["neg_updates"]
+            launches += st["kernel_launches"]
         t1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -710,6 +721,7 @@ def run_tournament(args):
                      "frac": value * bpu / 1e9 / world / peak, "traffic": None,
                      "bytes_per_update": bpu, "peak_source": peak_src,
                      "note": "whole-step average incl. exchanges, per GPU"},
+        "gpu_launches": launches,
         "clocks": clk.summary(),
     }
     if rank == 0:

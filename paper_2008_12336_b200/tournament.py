@@ -689,10 +689,16 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
             return t
         return t_prev
 
+    def launches():
+        return sum(f.sides.launches for f in {id(f): f for f in fns.values()}.values()) \
+            if has_prepare else 0
+
+    launches0 = launches()
     if use_graph:
         tp = time.perf_counter()
         upload(0)
         pr, sb = run_rotation(0, main0)
+        per_rotation = launches() - launches0
         tp = mark("eager_rotation", tp)
         # capture on a side stream with the bare capture API: torch.cuda.graph()
         # would also gc.collect() and empty the caching allocator on entry,
@@ -715,11 +721,13 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
         del graph
         mark("graph_destroy", tp)
         n_pairs, sent_bytes = pr * rotations, sb * rotations
+        n_launches = per_rotation * rotations
     else:
         for rot in range(rotations):
             pr, sb = run_rotation(rot, main0)
             n_pairs += pr
             sent_bytes += sb
+        n_launches = launches() - launches0
     store.drain()
     if store.device.type == "cuda":
         torch.cuda.current_stream(store.device).synchronize()
@@ -749,6 +757,7 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
         "neg_updates": neg,
         "exchange_bytes": sent_bytes,
         "train_s": train_s,
+        "kernel_launches": n_launches,  # this process's fill + pair kernels
         "part_device_bytes": store.device_bytes,
         **({"phases_s": phases} if phases else {}),
     }

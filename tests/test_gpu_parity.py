@@ -786,3 +786,21 @@ def test_device_negative_edges_equal_host(cuda, orc):
         h = gb.sample_negative_edges(g, 3000, seed, exclude_pairs=ex)
         d = gb.sample_negative_edges_device(g, 3000, seed, exclude_pairs=ex)
         assert np.array_equal(h, d)
+
+
+def test_host_register_failure_leaves_no_sticky_error(cuda):
+    """a failed gb_host_register (here: the range is already
+    registered) must not leave its error in the runtime's last-error slot,
+    where the next launch's check would report it (the pin_memory() fallback
+    of train_large relies on this)."""
+    a = np.zeros(1 << 20, dtype=np.float32)
+    L = _lib.load()
+    assert L.gb_host_register(a.ctypes.data, a.nbytes) == _lib.GB_OK
+    try:
+        assert L.gb_host_register(a.ctypes.data, a.nbytes) != _lib.GB_OK
+        x = torch.arange(1000, dtype=torch.int64, device="cuda")
+        out = torch.zeros(1, dtype=torch.int64, device="cuda")
+        _lib.call("gb_checksum", _lib.ptr(x), 1000, 8, _lib.ptr(out), _lib.stream())
+        torch.cuda.synchronize()
+    finally:
+        assert L.gb_host_unregister(a.ctypes.data) == _lib.GB_OK
