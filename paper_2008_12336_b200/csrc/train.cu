@@ -238,6 +238,21 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
       grid = (int)std::min<int64_t>(warps, (int64_t)num_sms() * std::max(occ1, 1));
       block = 32;
       smem = 0;
+    } else if (fn == var.pass && var.pass != var.pass_staged_hot && grid < num_sms()) {
+      // tiny levels (C3's coarsest: ~1.8K sources = 57 blocks of 256): the
+      // groups would sit on a third of the SMs; spread them over all SMs in
+      // smaller blocks (GB_SPREAD=0 keeps 256-thread blocks)
+      static const bool spread = [] {
+        const char *e = std::getenv("GB_SPREAD");
+        return !e || std::atoi(e) != 0;
+      }();
+      const int64_t gpw = kBlock / var.G / (kBlock / 32);  // groups per warp
+      const int64_t warps = std::max<int64_t>(1, (groups + gpw - 1) / gpw);
+      if (spread && warps > grid) {
+        const int64_t bw = std::max<int64_t>(1, std::min<int64_t>(8, warps / num_sms()));
+        block = (int)(32 * bw);
+        grid = (int)((warps + bw - 1) / bw);
+      }
     }
   } else {
     block = 32;

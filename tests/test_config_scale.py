@@ -56,6 +56,59 @@ def test_coarsening_matches_reference_checksums(cuda, shape):
             assert str(array_checksum(m.device_map())) == want["map"], ("map", L)
 
 
+_C4_CHILD = r"""
+import json, os, sys
+sys.path.insert(0, os.environ["GB_ROOT"])
+import paper_2008_12336_b200 as gb
+from paper_2008_12336_b200.graph import array_checksum
+gold = json.load(open(os.environ["GB_GOLD"]))
+gg = gold["graph"]
+g = gb.rmat_graph(gg["scale"], gg["samples"], gg["seed"], densify_ids=True)
+h = gb.coarsen_all(g, threshold=gold["threshold"])
+out = []
+for L, gl in enumerate(h.graphs):
+    x, a = gl.device_csr()
+    e = {"level": L, "vertices": gl.num_vertices, "arcs": gl.num_edges,
+         "xadj": str(array_checksum(x)), "adj": str(array_checksum(a[: gl.num_edges]))}
+    if L < len(h.mappings):
+        e["map"] = str(array_checksum(h.mappings[L].device_map()))
+        e["clusters"] = h.mappings[L].num_clusters
+    out.append(e)
+print(json.dumps({"stalled": bool(h.stalled), "levels": out}))
+"""
+
+
+def test_c4_shape_coarsening_matches_oracle_checksums(cuda):
+    """The north star's target shape (friendster-shaped R-MAT: 61.1M vertices,
+    3.74G arcs): the device hierarchy's per-level checksums equal the
+    oracle's sequential coarsen_all of the same CSR, computed on the GPU
+    box's host (scripts/c4_coarsen_parity.py; the oracle is pinned to the
+    reference's coarsen_all(num_workers=1)).  Runs in a child process with
+    the stream-ordered allocator (157 GiB peak)."""
+    import subprocess
+    import sys
+    path = os.path.join(GOLDEN, "coarsen_c4_hashes.json")
+    if not os.path.exists(path):
+        pytest.skip("C4 checksum golden not generated")
+    import gc
+
+    import torch
+    gc.collect()
+    torch.cuda.empty_cache()  # the child needs ~157 GiB of this process's GPU
+    if torch.cuda.mem_get_info()[0] < 165 << 30:
+        pytest.skip("needs ~165 GiB of free HBM (a 180 GB B200)")
+    with open(path) as f:
+        gold = json.load(f)
+    env = dict(os.environ, GB_ROOT=os.path.dirname(os.path.dirname(GOLDEN)), GB_GOLD=path,
+               PYTORCH_CUDA_ALLOC_CONF="backend:cudaMallocAsync")
+    r = subprocess.run([sys.executable, "-c", _C4_CHILD], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    assert got["stalled"] == gold["stalled"]
+    assert got["levels"] == gold["levels"]
+
+
 def test_checksum_matches_oracle(cuda, orc):
     rng = np.random.default_rng(3)
     for dt in (np.int32, np.int64):

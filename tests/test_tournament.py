@@ -203,13 +203,21 @@ def test_rotation_graph_deterministic_bit_exact(cuda, orc, G, monkeypatch):
     ref = M0.copy()
     rot = _sequential_replay(orc, g, x, a, ref, cfg, 60, G)
     assert rot >= 2
+    ref2 = ref.copy()
+    _sequential_replay(orc, g, x, a, ref2, cfg, 60, G)  # a second call's worth
     monkeypatch.setenv("GB_ROTATION_GRAPH", "1")  # from 2 rotations (auto: 16)
     for vs in ("1", "0"):
         monkeypatch.setenv("GB_VIRTUAL_STREAMS", vs)
+        tn.clear_rotation_graphs()
         M = torch.from_numpy(M0.copy()).cuda()
         st = tn.train_tournament(g, M, cfg, 60, num_ranks=G)
         assert st["rotations"] == rot and st["pairs"] == rot * (2 * G) * (2 * G + 1) // 2
         assert np.array_equal(M.cpu().numpy(), ref), vs
+        # the second call replays the cached graph for every rotation
+        assert len(tn._ROTATION_GRAPHS) == 1
+        st2 = tn.train_tournament(g, M, cfg, 60, num_ranks=G)
+        assert st2["pairs"] == st["pairs"] and st2["kernel_launches"] == st["kernel_launches"]
+        assert np.array_equal(M.cpu().numpy(), ref2), vs
 
 
 @pytest.mark.gpu
