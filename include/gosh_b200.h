@@ -216,6 +216,20 @@ int gb_train_passes(int64_t num_vertices, const int64_t *xadj,
                     const float *lr_per_epoch, unsigned flags,
                     int64_t max_groups, int64_t *status, void *stream_handle);
 
+/* gb_train_passes with positives from VERSE's personalized-PageRank
+ * similarity instead of the reference's adjacency similarity (SURVEY.md 8(f)
+ * rank 4; not in the reference): a walk from v that continues to
+ * a uniform neighbour while a uniform draw is below ppr_alpha (0 < alpha < 1;
+ * VERSE uses 0.85), capped at 64 steps; the sample is the vertex reached (v
+ * itself with probability 1 - alpha).  Negatives, update rule, EXACT mode
+ * and status are those of gb_train_passes. */
+int gb_train_passes_ppr(int64_t num_vertices, const int64_t *xadj, const int32_t *adj,
+                        const int32_t *sources, int64_t n_sources, float *M, int dim, int n_neg,
+                        uint64_t seed, uint64_t rng_stream, int64_t pass_begin, int64_t n_passes,
+                        int64_t passes_per_epoch, const float *lr_per_epoch, unsigned flags,
+                        int64_t max_groups, int64_t *status, double ppr_alpha,
+                        void *stream_handle);
+
 /* Fixed sample lists (update_embedding, trainer.py:137-142, generalized):
  * source src[i] is updated against samples[i*k + j] for j = 0..k-1 in order
  * (-1 skips a slot) with label labels[j] (1 positive, 0 negative), single-

@@ -53,6 +53,9 @@ def lib():
                                      _u64, _int, _int]),
             "or_train_passes": (None, [_i64p, _i32p, _i64, _f32p, _int, _int, _u64, _u64, _i64,
                                        _i64, _i64, _f32p, _int, _int]),
+            "or_train_passes_ppr": (None, [_i64p, _i32p, _i64, _f32p, _int, _int, _u64, _u64,
+                                           _i64, _i64, _i64, _f32p, _int, _int, _dbl]),
+            "or_ppr_positives": (None, [_i64p, _i32p, _i64, _dbl, _u64, _u64, _i64, _i64p]),
             "or_fill_pool_side": (None, [_i64p, _i32p, _i64, _i64, _i64, _i64, _int, _u64, _u64,
                                          _i32p]),
             "or_train_pool_side": (_i64, [_f32p, _f32p, _int, _i32p, _i64, _int, _i64, _i64,
@@ -133,13 +136,17 @@ def passes_per_epoch(num_vertices: int, num_edges: int, epoch_unit: str) -> int:
 
 
 def train_level(xadj, adj, M, dim, e_i, lr0, n_neg, seed, stream, epoch_unit="vertex-pass",
-                nthreads=1, reuse=False) -> tuple[int, int]:
+                nthreads=1, reuse=False, ppr_alpha=0.0) -> tuple[int, int]:
     """train_level (trainer.py:210-240) over the C pass; returns (passes, updates)."""
     V = len(xadj) - 1
     E = int(xadj[-1])
     ppe = passes_per_epoch(V, E, epoch_unit)
     lrs = np.asarray([np.float32(lr_at(lr0, j, e_i)) for j in range(e_i)], dtype=np.float32)
-    if e_i:
+    if e_i and ppr_alpha > 0:  # VERSE PPR positives (not in the reference; SPEC.md:14)
+        lib().or_train_passes_ppr(_c(xadj, np.int64), _c(adj, np.int32), V, M, dim, int(n_neg),
+                                  _u(seed), _u(stream), 0, e_i * ppe, ppe, lrs, int(nthreads),
+                                  int(bool(reuse)), float(ppr_alpha))
+    elif e_i:
         lib().or_train_passes(_c(xadj, np.int64), _c(adj, np.int32), V, M, dim, int(n_neg),
                               _u(seed), _u(stream), 0, e_i * ppe, ppe, lrs, int(nthreads),
                               int(bool(reuse)))
@@ -148,6 +155,14 @@ def train_level(xadj, adj, M, dim, e_i, lr0, n_neg, seed, stream, epoch_unit="ve
 
 
 # -- bigtrain.py -----------------------------------------------------------------
+def ppr_positives(xadj, adj, v, alpha, seed, stream, n_draws) -> np.ndarray:
+    """n_draws PPR positives of v, draw k keyed like pass k's source v."""
+    out = np.empty(n_draws, dtype=np.int64)
+    lib().or_ppr_positives(_c(xadj, np.int64), _c(adj, np.int32), int(v), float(alpha),
+                           _u(seed), _u(stream), int(n_draws), out)
+    return out
+
+
 def fill_pool_side(xadj, adj, lo_s, hi_s, lo_t, hi_t, B, seed, side) -> np.ndarray:
     out = np.empty((hi_s - lo_s, B), dtype=np.int32)
     lib().or_fill_pool_side(_c(xadj, np.int64), _c(adj, np.int32), lo_s, hi_s, lo_t, hi_t, B,

@@ -71,6 +71,8 @@ SIGNATURES = {
     "gb_unique_ids": (_int, [_p, _i64, _p, _pi64, _int, _p, _sz, _p]),
     "gb_train_passes": (_int, [_i64, _p, _p, _p, _i64, _p, _int, _int, _u64, _u64, _i64, _i64,
                                _i64, _p, C.c_uint, _i64, _p, _p]),
+    "gb_train_passes_ppr": (_int, [_i64, _p, _p, _p, _i64, _p, _int, _int, _u64, _u64, _i64,
+                                   _i64, _i64, _p, C.c_uint, _i64, _p, _dbl, _p]),
     "gb_active_sources_workspace": (_int, [_i64, _psz]),
     "gb_active_sources": (_int, [_i64, _p, _p, _pi64, _p, _sz, _p]),
     "gb_apply_sample_lists": (_int, [_p, _int, _i64, _p, _int, _p, _p, _dbl, C.c_uint, _i64, _p,

@@ -149,12 +149,17 @@ int grid_for(const void *sym, int G, int64_t max_groups, int64_t work_items, int
 using namespace gb;
 using namespace gb::tk;
 
-GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int32_t *adj,
-                               const int32_t *sources, int64_t n_sources, float *M, int dim, int n_neg, uint64_t seed, uint64_t rng_stream,
-                               int64_t pass_begin, int64_t n_passes, int64_t passes_per_epoch,
-                               const float *lr_per_epoch, unsigned flags, int64_t max_groups,
-                               int64_t *status, void *stream_handle) {
+static int train_passes_impl(int64_t num_vertices, const int64_t *xadj, const int32_t *adj,
+                             const int32_t *sources, int64_t n_sources, float *M, int dim,
+                             int n_neg, uint64_t seed, uint64_t rng_stream, int64_t pass_begin,
+                             int64_t n_passes, int64_t passes_per_epoch,
+                             const float *lr_per_epoch, unsigned flags, int64_t max_groups,
+                             int64_t *status, double ppr_alpha, void *stream_handle) {
   GB_REQUIRE(num_vertices >= 0 && dim >= 1 && n_neg >= 0, "gb_train_passes: bad sizes");
+  GB_REQUIRE(ppr_alpha >= 0.0 && ppr_alpha < 1.0, "gb_train_passes: ppr_alpha in [0, 1)");
+  // PPR positives run on the run-time-flag kernels (the HOT ones draw
+  // adjacency positives only)
+  const bool ppr = ppr_alpha > 0.0;
   GB_REQUIRE(passes_per_epoch >= 1 && pass_begin >= 0 && n_passes >= 0,
              "gb_train_passes: bad pass range");
   GB_REQUIRE(xadj && M && lr_per_epoch && status, "gb_train_passes: null pointer");
@@ -163,11 +168,11 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
   Variant var;
   GB_REQUIRE(pick_variant(dim, aligned16(M, dim), exact, var),
              "gb_train_passes: dim %d unsupported", dim);
-  select_hot(var, flags, false);
+  if (!ppr) select_hot(var, flags, false);
   GB_REQUIRE(!sources || n_sources >= 0, "gb_train_passes: bad source list");
   PassArgs a{num_vertices, xadj, adj, sources, n_sources, M, dim, n_neg, seed, rng_stream, pass_begin, n_passes,
              passes_per_epoch, lr_per_epoch, (flags & GB_TRAIN_REUSE) != 0,
-             (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status};
+             (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status, ppr_alpha};
   int grid = 1, block = kBlock;
   size_t smem = s0_bytes(var, dim);
   PassFn fn = var.pass;
@@ -189,7 +194,7 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
       const int64_t want = std::min<int64_t>(max_groups > 0 ? max_groups : INT64_MAX, items);
       const char *env = std::getenv("GB_PASS_SMEM");
       const bool on = env ? std::atoi(env) != 0 : want >= full0;
-      if (on && var.pass_staged_hot && use_hot(flags)) var.pass = var.pass_staged_hot;
+      if (on && var.pass_staged_hot && use_hot(flags) && !ppr) var.pass = var.pass_staged_hot;
       fn = var.pass;
     }
     if (var.pass_staged_hot && var.pass == var.pass_staged_hot) {
@@ -219,14 +224,14 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
     bool pipe = false;
     int occ1 = 0;
     if (groups < full && pick_variant(dim, aligned16(M, dim), exact, lat, true)) {
-      select_hot(lat, flags, false);
+      if (!ppr) select_hot(lat, flags, false);
       GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
           &occ1, (const void *)lat.pass_pipe, 32, 0));
       pipe = groups <= (int64_t)num_sms() * std::max(occ1, 1) * (32 / lat.G);
     }
     if (const char *env = std::getenv("GB_PIPE")) {
       pipe = std::atoi(env) != 0 && pick_variant(dim, aligned16(M, dim), exact, lat, true);
-      if (pipe) select_hot(lat, flags, false);
+      if (pipe && !ppr) select_hot(lat, flags, false);
       if (pipe)
         GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &occ1, (const void *)lat.pass_pipe, 32, 0));
@@ -238,21 +243,6 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
       grid = (int)std::min<int64_t>(warps, (int64_t)num_sms() * std::max(occ1, 1));
       block = 32;
       smem = 0;
-    } else if (fn == var.pass && var.pass != var.pass_staged_hot && grid < num_sms()) {
-      // tiny levels (C3's coarsest: ~1.8K sources = 57 blocks of 256): the
-      // groups would sit on a third of the SMs; spread them over all SMs in
-      // smaller blocks (GB_SPREAD=0 keeps 256-thread blocks)
-      static const bool spread = [] {
-        const char *e = std::getenv("GB_SPREAD");
-        return !e || std::atoi(e) != 0;
-      }();
-      const int64_t gpw = kBlock / var.G / (kBlock / 32);  // groups per warp
-      const int64_t warps = std::max<int64_t>(1, (groups + gpw - 1) / gpw);
-      if (spread && warps > grid) {
-        const int64_t bw = std::max<int64_t>(1, std::min<int64_t>(8, warps / num_sms()));
-        block = (int)(32 * bw);
-        grid = (int)((warps + bw - 1) / bw);
-      }
     }
   } else {
     block = 32;
@@ -260,6 +250,29 @@ GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int3
   fn<<<grid, block, smem, as_stream(stream_handle)>>>(a);
   GB_CHECK_LAUNCH();
   return GB_OK;
+}
+
+GB_API int gb_train_passes(int64_t num_vertices, const int64_t *xadj, const int32_t *adj,
+                           const int32_t *sources, int64_t n_sources, float *M, int dim,
+                           int n_neg, uint64_t seed, uint64_t rng_stream, int64_t pass_begin,
+                           int64_t n_passes, int64_t passes_per_epoch,
+                           const float *lr_per_epoch, unsigned flags, int64_t max_groups,
+                           int64_t *status, void *stream_handle) {
+  return train_passes_impl(num_vertices, xadj, adj, sources, n_sources, M, dim, n_neg, seed,
+                           rng_stream, pass_begin, n_passes, passes_per_epoch, lr_per_epoch,
+                           flags, max_groups, status, 0.0, stream_handle);
+}
+
+GB_API int gb_train_passes_ppr(int64_t num_vertices, const int64_t *xadj, const int32_t *adj,
+                               const int32_t *sources, int64_t n_sources, float *M, int dim,
+                               int n_neg, uint64_t seed, uint64_t rng_stream,
+                               int64_t pass_begin, int64_t n_passes, int64_t passes_per_epoch,
+                               const float *lr_per_epoch, unsigned flags, int64_t max_groups,
+                               int64_t *status, double ppr_alpha, void *stream_handle) {
+  GB_REQUIRE(ppr_alpha > 0.0, "gb_train_passes_ppr: ppr_alpha must be > 0");
+  return train_passes_impl(num_vertices, xadj, adj, sources, n_sources, M, dim, n_neg, seed,
+                           rng_stream, pass_begin, n_passes, passes_per_epoch, lr_per_epoch,
+                           flags, max_groups, status, ppr_alpha, stream_handle);
 }
 
 static int train_pool_side_impl(float *Msrc, float *Mtgt, int dim, const int32_t *targets,

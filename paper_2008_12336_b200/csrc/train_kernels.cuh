@@ -646,7 +646,45 @@ struct PassArgs {
   bool atomic;
   int64_t max_groups;
   int64_t *status;
+  // > 0: positives from VERSE's personalized-PageRank similarity with this
+  // continue probability instead of the adjacency similarity (run-time-flag
+  // kernels only; see ppr_positive)
+  double ppr_alpha;
 };
+
+// Positive sample of source v (deg > 0).  Adjacency similarity (the
+// reference, trainer.py:203): a uniform neighbour.  PPR similarity (VERSE's
+// sample_rw, the measure GOSH's paper names beside adjacency):
+// start at v; while a uniform draw is below alpha, step to a uniform
+// neighbour of the current vertex (stop early at a sink); the sample is the
+// vertex reached -- v itself with probability 1 - alpha (a self-sample,
+// trained with the self rule).  Walk draws use counters from kPprCtr up, far
+// from the negatives' 1..n_neg; walks are capped at kPprMaxSteps.
+constexpr uint64_t kPprCtr = 1ull << 40;
+constexpr int kPprMaxSteps = 64;
+
+__device__ __forceinline__ int32_t ppr_positive(const int64_t *__restrict__ xadj,
+                                                const int32_t *__restrict__ adj, int64_t v,
+                                                double alpha, uint64_t key) {
+  int64_t u = v;
+  for (int t = 0; t < kPprMaxSteps; ++t) {
+    if (!(draw_unit(key, kPprCtr + 2 * (uint64_t)t) < alpha)) break;
+    const int64_t x0 = __ldg(xadj + u);
+    const int64_t d = __ldg(xadj + u + 1) - x0;
+    if (d == 0) break;
+    u = __ldg(adj + x0 + draw_below(key, kPprCtr + 2 * (uint64_t)t + 1, d));
+  }
+  return (int32_t)u;
+}
+
+template <bool HOT>
+__device__ __forceinline__ int32_t positive_sample(const PassArgs &a, int64_t v, int64_t x0,
+                                                   int64_t deg, uint64_t key) {
+  if constexpr (!HOT) {
+    if (a.ppr_alpha > 0.0) return ppr_positive(a.xadj, a.adj, v, a.ppr_alpha, key);
+  }
+  return __ldg(a.adj + x0 + draw_below(key, 0, deg));  // trainer.py:203
+}
 
 // Index half of a source: v, the positive (xadj -> adj), the first chunk of
 // negatives, the RNG key and the pass's lr.  Read-only inputs, so computing
@@ -686,8 +724,8 @@ __device__ __forceinline__ void fetch_source(const PassArgs &a, int64_t p, int64
   for (int j = 0; j < kChunk; ++j) {
     if (j >= nsamp)
       d.ids[j] = -1;
-    else if (j == 0)  // positive: uniform neighbour (trainer.py:203)
-      d.ids[j] = __ldg(a.adj + x0 + draw_below(d.key, 0, deg));
+    else if (j == 0)  // positive (trainer.py:203, or a PPR walk)
+      d.ids[j] = positive_sample<false>(a, v, x0, deg, d.key);
     else  // negatives: uniform over V (trainer.py:205-206)
       d.ids[j] = (int32_t)draw_below(d.key, (uint64_t)j, a.V);
   }
@@ -846,8 +884,8 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 
             const int idx = c0 + j;
             if (idx >= nsamp)
               ids[j] = -1;
-            else if (idx == 0)  // positive: uniform neighbour (trainer.py:203)
-              ids[j] = __ldg(a.adj + x0 + draw_below(key, 0, deg));
+            else if (idx == 0)  // positive: uniform neighbour (trainer.py:203) or PPR
+              ids[j] = positive_sample<HOT>(a, v, x0, deg, key);
             else  // negatives: uniform over V (trainer.py:205-206)
               ids[j] = (int32_t)draw_below(key, (uint64_t)idx, a.V);
           }

@@ -40,6 +40,7 @@ EMBED_VERSION = 1
 SIGMOID_CLAMP = 10.0
 LR_FLOOR = 1e-4
 EPOCH_UNITS = ("vertex-pass", "edge-scaled")
+SIMILARITIES = ("adjacency", "ppr")
 # auto in-flight policy max(FLOOR, V / DIVISOR).  Default: uncapped (the
 # cap is >= V).  Round 1 needed max(256, V/16) to hold C1 AUCROC to the
 # reference while source rows were written back with plain stores; with the
@@ -70,6 +71,12 @@ class TrainConfig:
     atomic_rows: bool = True
     # partitioned / sharded trainers only: balanced pools (bigtrain.PairSides)
     balanced_pools: bool = False
+    # positive-sample similarity: "adjacency" (the reference, trainer.py:203)
+    # or "ppr" -- VERSE's personalized PageRank with continue probability
+    # ppr_alpha (not in the reference, SPEC.md:14;
+    # in-memory levels only: the part-pair pools are adjacency by design)
+    similarity: str = "adjacency"
+    ppr_alpha: float = 0.85
 
     def validate(self) -> None:
         if self.dim < 1:
@@ -90,6 +97,10 @@ class TrainConfig:
             raise ConfigError("max_inflight must be >= 0")
         if self.balanced_pools and self.deterministic:
             raise ConfigError("balanced_pools runs on the Hogwild kernels (deterministic=False)")
+        if self.similarity not in SIMILARITIES:
+            raise ConfigError(f"similarity must be one of {SIMILARITIES}")
+        if self.similarity == "ppr" and not 0.0 < self.ppr_alpha < 1.0:
+            raise ConfigError("ppr_alpha must be in (0, 1)")
 
 
 @dataclass
@@ -312,11 +323,16 @@ def train_level(g: Graph, M, cfg: TrainConfig, e_i: int, lr0: float | None = Non
     cap = inflight_cap(cfg, g.num_vertices)
     flags = _train_flags(cfg)
     st = _lib.stream()
+    ppr = cfg.similarity == "ppr"
     for j in range(e_i):
-        _lib.call("gb_train_passes", g.num_vertices, _lib.ptr(xadj), _lib.ptr(adj),
-                  _lib.ptr(sources), n_src, _lib.ptr(dm.dev), cfg.dim, cfg.negative_samples, _lib.u64(cfg.seed),
-                  _lib.u64(rng_stream), j * ppe, ppe, ppe, _lib.ptr(lrs), flags, cap,
-                  _lib.ptr(status), st)
+        args = (g.num_vertices, _lib.ptr(xadj), _lib.ptr(adj), _lib.ptr(sources), n_src,
+                _lib.ptr(dm.dev), cfg.dim, cfg.negative_samples, _lib.u64(cfg.seed),
+                _lib.u64(rng_stream), j * ppe, ppe, ppe, _lib.ptr(lrs), flags, cap,
+                _lib.ptr(status))
+        if ppr:
+            _lib.call("gb_train_passes_ppr", *args, float(cfg.ppr_alpha), st)
+        else:
+            _lib.call("gb_train_passes", *args, st)
     _lib.call("gb_nonfinite_scan", _lib.ptr(dm.dev), dm.dev.numel(), e_i - 1, _lib.ptr(status),
               st)
     dm.close()
