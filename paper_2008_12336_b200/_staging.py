@@ -81,3 +81,109 @@ def device_to_file(f, src: torch.Tensor) -> None:
         n = min(CHUNK, nbytes - k * CHUNK)
         f.write(memoryview(bufs[k % 2].numpy())[:n])
     src.record_stream(side)
+
+
+# ---------------------------------------------------------------------------
+# numpy <-> device arrays.  torch's .cuda() / .cpu() on pageable memory run at
+# ~11 / ~2.2 GB/s here (the download into fresh pages is page-fault bound:
+# 0.60 s for C3's 1.34 GB matrix, 64% of the end-to-end embed;
+# profiles/r02_c3_e2e_phases.jsonl).  These stage through the two pinned
+# chunks with the host-side copies split over a thread pool (numpy releases
+# the GIL for plain copies), so the page faults and memcpy run in parallel
+# while the next chunk's DMA is in flight.
+# ---------------------------------------------------------------------------
+_SMALL = 8 << 20  # below this, torch's own copy is as fast
+_pool_threads = None
+
+
+def _threads():
+    global _pool_threads
+    if _pool_threads is None:
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        _pool_threads = ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1)))
+    return _pool_threads
+
+
+def _par_copy(dst, src) -> None:
+    """dst[...] = src for two equal-length 1-D uint8 numpy views, in pieces."""
+    n = dst.shape[0]
+    ex = _threads()
+    k = ex._max_workers
+    step = -(-n // k)
+    futs = [ex.submit(dst.__setitem__, slice(i, min(i + step, n)), src[i:min(i + step, n)])
+            for i in range(0, n, step)]
+    for f in futs:
+        f.result()
+
+
+def numpy_to_device(a):
+    """A CUDA tensor with the contents of numpy array `a` (same dtype/shape)."""
+    import numpy as np
+    a = np.ascontiguousarray(a)
+    t = torch.from_numpy(a)
+    if a.nbytes < _SMALL:
+        return t.cuda()
+    out = torch.empty(t.shape, dtype=t.dtype, device="cuda")
+    src = a.reshape(-1).view(np.uint8)
+    dst = out.view(-1).view(torch.uint8)
+    bufs = _buffers()
+    main = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+    side.wait_stream(main)
+    done: list = [None, None]
+    n = src.shape[0]
+    off, k = 0, 0
+    while off < n:
+        m = min(CHUNK, n - off)
+        b = bufs[k % 2]
+        if done[k % 2] is not None:
+            done[k % 2].synchronize()
+        _par_copy(b.numpy()[:m], src[off:off + m])
+        with torch.cuda.stream(side):
+            dst[off:off + m].copy_(b[:m], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        done[k % 2] = ev
+        off += m
+        k += 1
+    main.wait_stream(side)
+    out.record_stream(side)
+    side.synchronize()
+    return out
+
+
+def device_to_numpy(t):
+    """A new numpy array with the contents of CUDA tensor `t`."""
+    import numpy as np
+    t = t.detach().contiguous()
+    if t.numel() * t.element_size() < _SMALL:
+        return t.cpu().numpy()
+    out = np.empty(tuple(t.shape), dtype=torch.empty(0, dtype=t.dtype).numpy().dtype)
+    dst = out.reshape(-1).view(np.uint8)
+    src = t.view(-1).view(torch.uint8)
+    n = dst.shape[0]
+    bufs = _buffers()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    pend = []
+    off, k = 0, 0
+    while off < n:
+        m = min(CHUNK, n - off)
+        b = bufs[k % 2]
+        with torch.cuda.stream(side):
+            b[:m].copy_(src[off:off + m], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        pend.append((ev, b, off, m))
+        if len(pend) == 2:  # drain the older chunk while this one is in flight
+            e, bb, o, mm = pend.pop(0)
+            e.synchronize()
+            _par_copy(dst[o:o + mm], bb.numpy()[:mm])
+        off += m
+        k += 1
+    for e, bb, o, mm in pend:
+        e.synchronize()
+        _par_copy(dst[o:o + mm], bb.numpy()[:mm])
+    t.record_stream(side)
+    return out

@@ -53,7 +53,8 @@ class Graph:
     @property
     def xadj(self) -> np.ndarray:
         if self._xadj is None:
-            self._xadj = self._xadj_dev.cpu().numpy()
+            from ._staging import device_to_numpy
+            self._xadj = device_to_numpy(self._xadj_dev)
         return self._xadj
 
     @xadj.setter
@@ -67,7 +68,8 @@ class Graph:
             if self._adj_dev is None:
                 self._adj = np.empty(0, dtype=np.int32)
             else:
-                self._adj = self._adj_dev[: self.num_edges].cpu().numpy()
+                from ._staging import device_to_numpy
+                self._adj = device_to_numpy(self._adj_dev[: self.num_edges])
         return self._adj
 
     @adj.setter
@@ -79,14 +81,14 @@ class Graph:
     def device_csr(self) -> tuple[torch.Tensor, torch.Tensor]:
         """(xadj int64[V+1], adj int32[max(E,1)]) on the current CUDA device."""
         _lib.require_cuda()
+        from ._staging import numpy_to_device
         if self._xadj_dev is None:
-            self._xadj_dev = torch.from_numpy(
-                np.ascontiguousarray(self._xadj, dtype=np.int64)).cuda()
+            self._xadj_dev = numpy_to_device(np.ascontiguousarray(self._xadj, dtype=np.int64))
         if self._adj_dev is None:
             a = np.ascontiguousarray(self.adj, dtype=np.int32)
             if a.size == 0:
                 a = np.zeros(1, dtype=np.int32)
-            self._adj_dev = torch.from_numpy(a).cuda()
+            self._adj_dev = numpy_to_device(a)
         return self._xadj_dev, self._adj_dev
 
     def active_sources(self) -> tuple[torch.Tensor, int]:

@@ -31,6 +31,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from ._staging import device_to_numpy, numpy_to_device
 from .coarsen import Hierarchy, Mapping, coarsen_all
 from .errors import ConfigError, PlanError
 from .graph import Graph
@@ -165,11 +166,11 @@ class _DeviceMatrix:
             if not isinstance(M, np.ndarray) or M.dtype != np.float32:
                 raise TypeError("embedding matrix must be float32")
             self.host = M
-            self.dev = torch.from_numpy(np.ascontiguousarray(M)).cuda()
+            self.dev = numpy_to_device(M)
 
     def close(self) -> None:
         if self.host is not None:
-            self.host[...] = self.dev.cpu().numpy()
+            self.host[...] = device_to_numpy(self.dev)
         elif self.host_tensor is not None:
             self.host_tensor.copy_(self.dev, non_blocking=True)
             torch.cuda.current_stream().synchronize()
@@ -391,7 +392,7 @@ def train_multilevel(g0: Graph, cfg: TrainConfig, budget=None, threshold: int = 
                 train_large(g_i, M, cfg, e_i, budget, rng_stream=i)
         if i > 0:
             M = expand_embedding(M, hierarchy.mappings[i - 1])
-    return M if return_device else M.cpu().numpy()
+    return M if return_device else device_to_numpy(M)
 
 
 # ---------------------------------------------------------------------------

@@ -152,3 +152,24 @@ def test_gshe_round_trip_through_pinned_staging(cuda, tmp_path, monkeypatch):
     D = gb.load_embedding(p1, device=True)
     assert D.is_cuda and torch.equal(D, M)
     assert np.array_equal(gb.load_embedding(p1), M.cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_staged_array_transfers_round_trip(cuda, monkeypatch):
+    """numpy <-> device through the pinned chunks with threaded host copies
+    (Graph uploads/downloads, train_multilevel's result): exact, for sizes
+    that are not multiples of the chunk."""
+    import torch
+    from paper_2008_12336_b200 import _staging
+    monkeypatch.setattr(_staging, "CHUNK", 4096)
+    monkeypatch.setattr(_staging, "_SMALL", 0)
+    monkeypatch.setattr(_staging, "_pool", [])
+    rng = np.random.default_rng(2)
+    for a in (rng.standard_normal((1000, 33)).astype(np.float32),
+              rng.integers(-2**62, 2**62, size=12_345),
+              rng.integers(0, 2**31 - 1, size=(7, 999), dtype=np.int32)):
+        d = _staging.numpy_to_device(a)
+        assert d.is_cuda and d.dtype == torch.from_numpy(a).dtype
+        assert np.array_equal(d.cpu().numpy(), a)
+        back = _staging.device_to_numpy(d)
+        assert back.dtype == a.dtype and np.array_equal(back, a)
