@@ -221,8 +221,9 @@ int gb_train_passes(int64_t num_vertices, const int64_t *xadj,
  * rank 4; not in the reference): a walk from v that continues to
  * a uniform neighbour while a uniform draw is below ppr_alpha (0 < alpha < 1;
  * VERSE uses 0.85), capped at 64 steps; the sample is the vertex reached (v
- * itself with probability 1 - alpha).  Negatives, update rule, EXACT mode
- * and status are those of gb_train_passes. */
+ * itself with probability 1 - alpha).  alpha is used rounded to float32.
+ * Negatives, update rule, EXACT mode and status are those of
+ * gb_train_passes. */
 int gb_train_passes_ppr(int64_t num_vertices, const int64_t *xadj, const int32_t *adj,
                         const int32_t *sources, int64_t n_sources, float *M, int dim, int n_neg,
                         uint64_t seed, uint64_t rng_stream, int64_t pass_begin, int64_t n_passes,

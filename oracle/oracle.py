@@ -145,7 +145,7 @@ def train_level(xadj, adj, M, dim, e_i, lr0, n_neg, seed, stream, epoch_unit="ve
     if e_i and ppr_alpha > 0:  # VERSE PPR positives (not in the reference)
         lib().or_train_passes_ppr(_c(xadj, np.int64), _c(adj, np.int32), V, M, dim, int(n_neg),
                                   _u(seed), _u(stream), 0, e_i * ppe, ppe, lrs, int(nthreads),
-                                  int(bool(reuse)), float(ppr_alpha))
+                                  int(bool(reuse)), float(np.float32(ppr_alpha)))
     elif e_i:
         lib().or_train_passes(_c(xadj, np.int64), _c(adj, np.int32), V, M, dim, int(n_neg),
                               _u(seed), _u(stream), 0, e_i * ppe, ppe, lrs, int(nthreads),
@@ -158,7 +158,9 @@ def train_level(xadj, adj, M, dim, e_i, lr0, n_neg, seed, stream, epoch_unit="ve
 def ppr_positives(xadj, adj, v, alpha, seed, stream, n_draws) -> np.ndarray:
     """n_draws PPR positives of v, draw k keyed like pass k's source v."""
     out = np.empty(n_draws, dtype=np.int64)
-    lib().or_ppr_positives(_c(xadj, np.int64), _c(adj, np.int32), int(v), float(alpha),
+    # alpha as the device holds it (float32, train_kernels.cuh PassArgs)
+    lib().or_ppr_positives(_c(xadj, np.int64), _c(adj, np.int32), int(v),
+                           float(np.float32(alpha)),
                            _u(seed), _u(stream), int(n_draws), out)
     return out
 

@@ -122,7 +122,7 @@ def numpy_to_device(a):
     import numpy as np
     a = np.ascontiguousarray(a)
     t = torch.from_numpy(a)
-    if a.nbytes < _SMALL:
+    if a.nbytes < _SMALL or t.is_pinned():  # page-locked already: one direct DMA
         return t.cuda()
     out = torch.empty(t.shape, dtype=t.dtype, device="cuda")
     src = a.reshape(-1).view(np.uint8)

@@ -172,7 +172,8 @@ static int train_passes_impl(int64_t num_vertices, const int64_t *xadj, const in
   GB_REQUIRE(!sources || n_sources >= 0, "gb_train_passes: bad source list");
   PassArgs a{num_vertices, xadj, adj, sources, n_sources, M, dim, n_neg, seed, rng_stream, pass_begin, n_passes,
              passes_per_epoch, lr_per_epoch, (flags & GB_TRAIN_REUSE) != 0,
-             (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0, exact ? 1 : max_groups, status, ppr_alpha};
+             (flags & GB_TRAIN_FAST_SIGMOID) != 0, !exact && (flags & GB_TRAIN_ATOMIC) != 0,
+             (float)ppr_alpha, exact ? 1 : max_groups, status};
   int grid = 1, block = kBlock;
   size_t smem = s0_bytes(var, dim);
   PassFn fn = var.pass;

@@ -644,12 +644,14 @@ struct PassArgs {
   bool reuse;
   bool fast;
   bool atomic;
-  int64_t max_groups;
-  int64_t *status;
   // > 0: positives from VERSE's personalized-PageRank similarity with this
   // continue probability instead of the adjacency similarity (run-time-flag
-  // kernels only; see ppr_positive)
-  double ppr_alpha;
+  // kernels only; see ppr_positive).  float, in the bools' padding: growing
+  // the struct changed ptxas's allocation of the HOT KIND 3 pass (stack 24
+  // -> 40 bytes, -5% on C2)
+  float ppr_alpha;
+  int64_t max_groups;
+  int64_t *status;
 };
 
 // Positive sample of source v (deg > 0).  Adjacency similarity (the
@@ -681,7 +683,7 @@ template <bool HOT>
 __device__ __forceinline__ int32_t positive_sample(const PassArgs &a, int64_t v, int64_t x0,
                                                    int64_t deg, uint64_t key) {
   if constexpr (!HOT) {
-    if (a.ppr_alpha > 0.0) return ppr_positive(a.xadj, a.adj, v, a.ppr_alpha, key);
+    if (a.ppr_alpha > 0.0f) return ppr_positive(a.xadj, a.adj, v, (double)a.ppr_alpha, key);
   }
   return __ldg(a.adj + x0 + draw_below(key, 0, deg));  // trainer.py:203
 }

@@ -48,7 +48,8 @@ for rep in range(3):
         if i > 0:
             M = gb.expand_embedding(M, h.mappings[i - 1])
             t = mark("expand", t)
-    out = M.cpu().numpy()
+    from paper_2008_12336_b200._staging import device_to_numpy
+    out = device_to_numpy(M)  # train_multilevel's download
     t = mark("download", t)
     ph["total"] = time.perf_counter() - t0
     print(json.dumps({"rep": rep, "unit": UNIT, "phases_s": {k: round(v, 4) for k, v in ph.items()},
