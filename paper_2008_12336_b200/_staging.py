@@ -117,16 +117,16 @@ def _par_copy(dst, src) -> None:
         f.result()
 
 
-def numpy_to_device(a):
-    """A CUDA tensor with the contents of numpy array `a` (same dtype/shape)."""
+def copy_numpy_to_device(dst, a) -> None:
+    """dst (contiguous CUDA tensor) <- numpy array a (same number of bytes)."""
     import numpy as np
     a = np.ascontiguousarray(a)
     t = torch.from_numpy(a)
     if a.nbytes < _SMALL or t.is_pinned():  # page-locked already: one direct DMA
-        return t.cuda()
-    out = torch.empty(t.shape, dtype=t.dtype, device="cuda")
+        dst.view(-1).view(torch.uint8).copy_(t.reshape(-1).view(torch.uint8))
+        return
     src = a.reshape(-1).view(np.uint8)
-    dst = out.view(-1).view(torch.uint8)
+    dst = dst.view(-1).view(torch.uint8)
     bufs = _buffers()
     main = torch.cuda.current_stream()
     side = torch.cuda.Stream()
@@ -148,21 +148,29 @@ def numpy_to_device(a):
         off += m
         k += 1
     main.wait_stream(side)
-    out.record_stream(side)
+    dst.record_stream(side)
     side.synchronize()
+
+
+def numpy_to_device(a):
+    """A CUDA tensor with the contents of numpy array `a` (same dtype/shape)."""
+    import numpy as np
+    a = np.ascontiguousarray(a)
+    out = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device="cuda")
+    copy_numpy_to_device(out, a)
     return out
 
 
-def device_to_numpy(t):
-    """A new numpy array with the contents of CUDA tensor `t`."""
+def copy_device_to_numpy(dst, t) -> None:
+    """numpy array dst (C-contiguous) <- CUDA tensor t (same number of bytes)."""
     import numpy as np
     t = t.detach().contiguous()
-    if t.numel() * t.element_size() < _SMALL:
-        return t.cpu().numpy()
-    out = np.empty(tuple(t.shape), dtype=torch.empty(0, dtype=t.dtype).numpy().dtype)
-    dst = out.reshape(-1).view(np.uint8)
+    dst8 = dst.reshape(-1).view(np.uint8)
+    if dst8.nbytes < _SMALL or torch.from_numpy(dst8).is_pinned():
+        torch.from_numpy(dst8).copy_(t.view(-1).view(torch.uint8))
+        return
     src = t.view(-1).view(torch.uint8)
-    n = dst.shape[0]
+    n = dst8.shape[0]
     bufs = _buffers()
     side = torch.cuda.Stream()
     side.wait_stream(torch.cuda.current_stream())
@@ -179,11 +187,18 @@ def device_to_numpy(t):
         if len(pend) == 2:  # drain the older chunk while this one is in flight
             e, bb, o, mm = pend.pop(0)
             e.synchronize()
-            _par_copy(dst[o:o + mm], bb.numpy()[:mm])
+            _par_copy(dst8[o:o + mm], bb.numpy()[:mm])
         off += m
         k += 1
     for e, bb, o, mm in pend:
         e.synchronize()
-        _par_copy(dst[o:o + mm], bb.numpy()[:mm])
+        _par_copy(dst8[o:o + mm], bb.numpy()[:mm])
     t.record_stream(side)
+
+
+def device_to_numpy(t):
+    """A new numpy array with the contents of CUDA tensor `t`."""
+    import numpy as np
+    out = np.empty(tuple(t.shape), dtype=torch.empty(0, dtype=t.dtype).numpy().dtype)
+    copy_device_to_numpy(out, t)
     return out

@@ -269,8 +269,12 @@ class PartStore:
 
     # -- filling ---------------------------------------------------------------
     def load_full(self, Mt: torch.Tensor) -> None:
+        from ._staging import copy_numpy_to_device
         for p, lo, hi, buf in self.local_parts():
-            buf.copy_(Mt[lo:hi], non_blocking=True)
+            if Mt.device.type == "cpu" and buf.is_cuda and not Mt.is_pinned():
+                copy_numpy_to_device(buf[: hi - lo], Mt[lo:hi].numpy())  # pinned chunks
+            else:
+                buf.copy_(Mt[lo:hi], non_blocking=True)
 
     def init_random(self, seed: int) -> None:
         """init_embedding(V, d, seed) restricted to the held rows."""
@@ -318,8 +322,12 @@ class PartStore:
                     lo, hi = self.rows(p)
                     out[lo:hi].copy_(bufs[rr // m][2 * (rr % m) + slot][: hi - lo])
         else:
+            from ._staging import copy_device_to_numpy
             for p, lo, hi, buf in self.local_parts():
-                out[lo:hi].copy_(buf)
+                if out.device.type == "cpu" and buf.is_cuda and not out.is_pinned():
+                    copy_device_to_numpy(out[lo:hi].numpy(), buf[: hi - lo])
+                else:
+                    out[lo:hi].copy_(buf)
         return out
 
     # -- pair views ----------------------------------------------------------------
@@ -868,7 +876,7 @@ def train_tournament(g: Graph, M, cfg: TrainConfig, e_i: int, batch_size: int = 
                                 rng_stream=rng_stream, group=group, pair_fn=pair_fn)
     if gather:
         store.to_full(out=Mt, group=group, distributed=distributed, device=Mt.device)
-        if not isinstance(M, torch.Tensor):
+        if not isinstance(M, torch.Tensor) and not np.shares_memory(M, Mt.numpy()):
             M[...] = Mt.numpy()
         if not bool(torch.isfinite(Mt).all()):
             raise FloatingPointError("non-finite embedding after tournament training")

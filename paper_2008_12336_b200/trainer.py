@@ -31,7 +31,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._staging import device_to_numpy, numpy_to_device
+from ._staging import copy_device_to_numpy, device_to_numpy, numpy_to_device
 from .coarsen import Hierarchy, Mapping, coarsen_all
 from .errors import ConfigError, PlanError
 from .graph import Graph
@@ -170,7 +170,10 @@ class _DeviceMatrix:
 
     def close(self) -> None:
         if self.host is not None:
-            self.host[...] = device_to_numpy(self.dev)
+            if self.host.flags.c_contiguous:
+                copy_device_to_numpy(self.host, self.dev)
+            else:
+                self.host[...] = device_to_numpy(self.dev)
         elif self.host_tensor is not None:
             self.host_tensor.copy_(self.dev, non_blocking=True)
             torch.cuda.current_stream().synchronize()
