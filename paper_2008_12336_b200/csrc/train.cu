@@ -109,33 +109,17 @@ void select_hot(Variant &v, unsigned flags, bool diagonal, bool pool_materialize
   PoolFn p = pool_balanced ? (diagonal ? v.pool_bal_hot_diag : v.pool_bal_hot)
                            : (diagonal ? v.pool_hot_diag : v.pool_hot);
   if (p && (pool_materialized || pool_balanced)) v.pool = p;
-  // staged pair kernels (GB_POOL_STAGED: 1 on, 0 off)
-  static const int staged_env = [] {
-    const char *e = std::getenv("GB_POOL_STAGED");
-    return e ? std::atoi(e) : -1;
-  }();
-  PoolFn ps = pool_balanced ? (diagonal ? v.pool_bal_hot_diag_st : v.pool_bal_hot_st)
-                            : (diagonal ? v.pool_hot_diag_st : v.pool_hot_st);
-  if (ps && v.pool == p && staged_env > 0) {
-    v.pool = ps;
-    v.pool_staged = true;
-  }
 }
 
 // Dynamic shared memory of a KIND 0/2 pass or pair-side launch: one slot per
 // group for the source's initial copy (SrcKeep) on vector layouts.
 size_t s0_bytes(const Variant &var, int dim) {
-  if (var.pool_staged) return (size_t)(kBlock / var.G) * kChunk * dim * sizeof(float);
   return var.s0_smem ? (size_t)(kBlock / var.G) * dim * sizeof(float) : 0;
 }
 
 // Launch of a pair-side kernel.
 int launch_pool(const Variant &var, const PoolArgs &a, int grid, cudaStream_t st) {
-  const size_t smem = s0_bytes(var, a.dim);
-  if (smem > 48 * 1024)
-    GB_CUDA_TRY(cudaFuncSetAttribute((const void *)var.pool,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  var.pool<<<grid, kBlock, smem, st>>>(a);
+  var.pool<<<grid, kBlock, s0_bytes(var, a.dim), st>>>(a);
   GB_CHECK_LAUNCH();
   return GB_OK;
 }
@@ -147,9 +131,6 @@ bool aligned16(const void *p, int dim) {
 int grid_for(const void *sym, int G, int64_t max_groups, int64_t work_items, int *grid,
              size_t smem = 0) {
   int occ = 0;
-  if (smem > 48 * 1024)  // the occupancy query honours the opt-in limit only once set
-    GB_CUDA_TRY(cudaFuncSetAttribute(sym, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
   GB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sym, kBlock, smem));
   if (occ < 1) occ = 1;
   const int64_t groups_per_block = kBlock / G;

@@ -1096,14 +1096,8 @@ __device__ __forceinline__ int64_t lower_bound_adj(const int32_t *__restrict__ a
 // flat samples l, l + G, ... of the window (the positive from the pool or the
 // CSR, a negative from the counter-based key), and the chunks take them by
 // shuffle -- the RNG runs once per sample instead of once per lane.
-// STAGED (HOT modes, vector layouts): the chunk's sample rows 1..3 are
-// cp.async-staged into the group's shared slots and loaded into registers
-// one at a time (run_chunk_staged, as the KIND 3 pass), so the kernel fits
-// 80 registers and 3 blocks per SM instead of holding four rows in
-// registers at 128 (2 blocks per SM).
-template <class Row, bool EXACT, int MODE, bool STAGED = false>
-__global__ void __launch_bounds__(kBlock, EXACT ? 1 : (STAGED ? 3 : Row::kMinBlocks))
-    train_pool_kernel(PoolArgs a) {
+template <class Row, bool EXACT, int MODE>
+__global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_pool_kernel(PoolArgs a) {
   constexpr int G = Row::G;
   constexpr int kWin = 2 * kChunk;
   // the source's initial copy in a shared slot per group (kBlock / G * dim
@@ -1156,8 +1150,7 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : (STAGED ? 3 : Row::kMinBlo
     }
     const uint64_t key = stream_key(seed, a.side, 1, (uint64_t)i);
     Row S;
-    float *slots = STAGED ? group_smem<Row>(kChunk * a.dim) : nullptr;  // slot 0 = S0
-    SrcKeep<Row, kS0Smem> keep(kS0Smem ? (STAGED ? slots : group_smem<Row>(a.dim)) : nullptr);
+    SrcKeep<Row, kS0Smem> keep(kS0Smem ? group_smem<Row>(a.dim) : nullptr);
     bool loaded = false;
     // lane's samples of window c0 (ids, -1 = none) and the window's positive
     // bits.  (An L2 prefetch of the next window's rows was measured and
@@ -1232,12 +1225,8 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : (STAGED ? 3 : Row::kMinBlo
         pos_count += __popc(pos_mask);
         neg_count += (ids[0] >= 0) + (ids[1] >= 0) + (ids[2] >= 0) + (ids[3] >= 0) -
                      __popc(pos_mask);
-        if constexpr (STAGED)
-          run_chunk_staged<Row>(S, i, ids, pos_mask, a.Mtgt, a.dim, lr, slots, g, bad, fast,
-                                atomic, diagonal, true);
-        else
-          run_chunk<Row, EXACT>(S, i, ids, pos_mask, a.Mtgt, a.dim, lr, reuse, diagonal, true,
-                                g, bad, fast, atomic);
+        run_chunk<Row, EXACT>(S, i, ids, pos_mask, a.Mtgt, a.dim, lr, reuse, diagonal, true, g,
+                              bad, fast, atomic);
       }
     }
     if (loaded) keep.writeback(S, a.Msrc + i * (int64_t)a.dim, g.gl, a.dim, atomic && !EXACT);
@@ -1329,12 +1318,6 @@ struct Variant {
   PoolFn pool_hot_diag = nullptr;  // diagonal pair (Msrc == Mtgt)
   PoolFn pool_bal_hot = nullptr;   // balanced pools
   PoolFn pool_bal_hot_diag = nullptr;
-  // the same four with staged rows (STAGED); pool_staged marks the selection
-  PoolFn pool_hot_st = nullptr;
-  PoolFn pool_hot_diag_st = nullptr;
-  PoolFn pool_bal_hot_st = nullptr;
-  PoolFn pool_bal_hot_diag_st = nullptr;
-  bool pool_staged = false;
 };
 
 template <class Row, bool EXACT, bool WITH_HOT = false>
@@ -1355,12 +1338,6 @@ Variant make_variant() {
     v.pool_hot_diag = train_pool_kernel<Row, false, 2>;
     v.pool_bal_hot = train_pool_kernel<Row, false, 3>;
     v.pool_bal_hot_diag = train_pool_kernel<Row, false, 4>;
-    if constexpr (Row::kStageable) {
-      v.pool_hot_st = train_pool_kernel<Row, false, 1, true>;
-      v.pool_hot_diag_st = train_pool_kernel<Row, false, 2, true>;
-      v.pool_bal_hot_st = train_pool_kernel<Row, false, 3, true>;
-      v.pool_bal_hot_diag_st = train_pool_kernel<Row, false, 4, true>;
-    }
   }
   return v;
 }
