@@ -123,6 +123,17 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def _max_over_ranks(t):
+    """all_reduce MAX (gloo takes host tensors: staged)."""
+    import torch
+    if torch.distributed.get_backend() == "gloo" and t.is_cuda:
+        h = t.cpu()
+        torch.distributed.all_reduce(h, op=torch.distributed.ReduceOp.MAX)
+        return h.to(t.device)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return t
+
+
 def dist_init():
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -130,8 +141,16 @@ def dist_init():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # GB_DIST_BACKEND=gloo: a functional check of the multi-rank path on a
+        # box with fewer GPUs than ranks (ranks share devices round-robin);
+        # timing such a run means nothing
+        backend = os.environ.get("GB_DIST_BACKEND", "nccl")
+        dev = local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, world, local
@@ -246,7 +265,7 @@ def run_ours(args):
     kern_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t = _max_over_ranks(t)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     upd_per_step = non_iso * (1 + NNEG)
@@ -282,7 +301,7 @@ def run_ours(args):
     e2e_s = time.perf_counter() - te
     if world > 1:
         t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t = _max_over_ranks(t)
         e2e_s = float(t.item())
     e2e_value = world * e2e_upd / e2e_s
     ppe = gb.trainer.passes_per_epoch(G, cfg)
@@ -523,7 +542,7 @@ def sharded_c3(args, rank, world, print_line=True):
     exch_ms = sum(a.elapsed_time(b) for a, b in events)
     if world > 1:
         t = torch.tensor([total_ms, exch_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t = _max_over_ranks(t)
         total_ms, exch_ms = (float(x) for x in t.tolist())
     value = upd / (total_ms / 1000.0)  # updates are summed over ranks by the driver
     bpu = 8 * C3_DIM + (8 * C3_DIM) / (SH_B * (1 + NNEG))
@@ -571,7 +590,7 @@ def run_sharded(args):
     e2e_s = time.perf_counter() - te
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t = _max_over_ranks(t)
         e2e_s = float(t.item())
     K = 2 * world
     part_bytes = -(-g.num_vertices // K) * C3_DIM * 4
@@ -698,7 +717,7 @@ def run_tournament(args):
     total_ms = t0.elapsed_time(t1)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t = _max_over_ranks(t)
         total_ms = float(t.item())
     value = upd / (total_ms / 1000.0)  # pos_updates are already summed over ranks
     bpu = 8 * dim + (8 * dim) / (B * (1 + NNEG))

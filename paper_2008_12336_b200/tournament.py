@@ -374,6 +374,10 @@ class PartStore:
         if m:
             import torch.distributed as dist
             self.drain()
+        # gloo moves host tensors only: with device parts (one GPU shared by
+        # test processes) the transfers are staged through host copies
+        wire = (torch.device("cpu") if m and self.device.type == "cuda"
+                and dist.get_backend(group) == "gloo" else self.device)
         for sr, ss, dr, ds in moves:
             part = hold[sr][ss]
             if sr in local and dr in local:
@@ -382,8 +386,8 @@ class PartStore:
                     sent += row_bytes
             elif sr in local:
                 buf = self.data[part]
-                if self.host:  # sends go out of HBM
-                    buf = buf.to(self.device, non_blocking=True)
+                if buf.device != wire:  # host parts to HBM (NCCL); device parts to host (gloo)
+                    buf = buf.to(wire)
                 ops.append(dist.P2POp(dist.isend, buf, dr // m, group))
                 sent += buf.numel() * buf.element_size()
                 gone.append(part)
@@ -391,7 +395,8 @@ class PartStore:
                 if not self.spare:
                     self.spare.append(self._alloc())
                 buf = self.spare.pop()
-                rbuf = torch.empty_like(buf, device=self.device) if self.host else buf
+                rbuf = buf if buf.device == wire else torch.empty(buf.shape, dtype=buf.dtype,
+                                                                  device=wire)
                 ops.append(dist.P2POp(dist.irecv, rbuf, sr // m, group))
                 arrived.append((part, buf, rbuf))
                 new[dr][ds] = part
@@ -922,6 +927,17 @@ def shard_plan(num_rows: int, dim: int, world: int, budget_bytes: int,
     return G, (m if distributed else G), True
 
 
+def _broadcast(M: torch.Tensor, group) -> None:
+    """rank 0's M to every rank (gloo: staged through the host)."""
+    import torch.distributed as dist
+    if M.is_cuda and dist.get_backend(group) == "gloo":
+        h = M.cpu()
+        dist.broadcast(h, 0, group=group)
+        M.copy_(h)
+    else:
+        dist.broadcast(M, 0, group=group)
+
+
 def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
                              shard_levels: int = 2, batch_size: int = 5, group=None,
                              num_ranks: int | None = None, hierarchy=None,
@@ -1022,7 +1038,7 @@ def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
         if sharded(i - 1):
             if store is None:  # first sharded level: from the replicated coarse matrix
                 if distributed and not broadcast_done:
-                    dist.broadcast(M, 0, group=group)
+                    _broadcast(M, group)
                     broadcast_done = True
                 coarse = M
             else:              # coarser level sharded too: gather it (it is ~5x smaller)
@@ -1042,5 +1058,5 @@ def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
             return store, stats
         M = store.to_full(group=group, distributed=distributed)
     elif distributed and not broadcast_done:
-        dist.broadcast(M, 0, group=group)
+        _broadcast(M, group)
     return (M if return_device else M.cpu().numpy()), stats

@@ -15,6 +15,7 @@ import torch  # noqa: E402
 import paper_2008_12336_b200 as gb  # noqa: E402
 
 LEVEL = int(os.environ.get("LEVEL", "4"))
+EPOCHS = int(os.environ.get("EPOCHS", "1"))
 g = gb.rmat_graph(22, 126_000_000, 7, densify_ids=True)
 h = gb.coarsen_all(g, threshold=100)
 gl = h.graphs[LEVEL]
@@ -22,9 +23,13 @@ cfg = gb.TrainConfig(dim=128, negative_samples=3, seed=1, epoch_unit="edge-scale
 M = torch.from_numpy(gb.init_embedding(gl.num_vertices, 128, 1)).cuda()
 torch.cuda.synchronize()
 t0 = time.perf_counter()
-st = gb.train_level(gl, M, cfg, 1, rng_stream=LEVEL)
+if EPOCHS > 1:  # warm-up launch
+    gb.train_level(gl, M, cfg, 1, rng_stream=LEVEL)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+st = gb.train_level(gl, M, cfg, EPOCHS, rng_stream=LEVEL)
 torch.cuda.synchronize()
 dt = time.perf_counter() - t0
-print(json.dumps({"level": LEVEL, "V": gl.num_vertices, "arcs": gl.num_edges,
+print(json.dumps({"level": LEVEL, "epochs": EPOCHS, "GB_PIPE": os.environ.get("GB_PIPE"), "V": gl.num_vertices, "arcs": gl.num_edges,
                   "passes": st.passes, "updates": st.updates, "s": dt,
                   "upd_per_s": st.updates / dt}))

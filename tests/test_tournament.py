@@ -405,3 +405,77 @@ def test_nccl_process_group_path_equals_virtual_ranks(cuda, orc):
         ref, _ = gb.train_multilevel_sharded(g, cfg, num_ranks=world)
         for r in range(world):
             assert np.array_equal(np.load(f"{out}.{r}.npy"), ref)
+
+
+def _gloo_gpu_worker(rank, world, port, out_path, what):
+    """Processes sharing cuda:0 over gloo: the distributed device code path
+    (device pair kernels, P2P shifts staged through the host, all_gather,
+    all_reduce, broadcast) when only one GPU is present."""
+    import torch.distributed as dist
+    from oracle import oracle as orc
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g, x, a = _graph(orc, scale=10, samples=6000)
+        if what == "tournament":
+            cfg = gb.TrainConfig(dim=32, negative_samples=3, seed=4, deterministic=True)
+            M = torch.from_numpy(orc.init_embedding(g.num_vertices, 32, 2)).cuda()
+            st = tn.train_tournament(g, M, cfg, 20)
+            np.save(f"{out_path}.{rank}.npy", M.cpu().numpy())
+            np.save(f"{out_path}.{rank}.sent.npy", np.array([st["exchange_bytes"]]))
+        else:
+            cfg = gb.TrainConfig(dim=32, total_epochs=30, negative_samples=3, seed=4,
+                                 deterministic=True)
+            M, _ = gb.train_multilevel_sharded(g, cfg)
+            np.save(f"{out_path}.{rank}.npy", M)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_processes_on_one_gpu_tournament(cuda, orc, world):
+    """world processes x one rank each on the one GPU (K = 2 world parts):
+    every off-diagonal round ends with a real cross-process part shift; the
+    result equals the sequential replay bit for bit on every rank."""
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "m")
+        mp.spawn(_gloo_gpu_worker, args=(world, port, out, "tournament"), nprocs=world,
+                 join=True)
+        g, x, a = _graph(orc, scale=10, samples=6000)
+        cfg = gb.TrainConfig(dim=32, negative_samples=3, seed=4, deterministic=True)
+        ref = orc.init_embedding(g.num_vertices, 32, 2)
+        _sequential_replay(orc, g, x, a, ref, cfg, 20, world)
+        for r in range(world):
+            assert np.array_equal(np.load(f"{out}.{r}.npy"), ref), r
+            assert int(np.load(f"{out}.{r}.sent.npy")[0]) > 0
+
+
+@pytest.mark.gpu
+def test_gloo_processes_on_one_gpu_sharded_multilevel(cuda, orc):
+    """train_multilevel_sharded over two processes (broadcast of the coarse
+    matrix, expand into parts, two sharded levels, all_gather) equals the
+    in-process virtual-rank run bit for bit."""
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "m")
+        mp.spawn(_gloo_gpu_worker, args=(2, port, out, "multilevel"), nprocs=2, join=True)
+        g, x, a = _graph(orc, scale=10, samples=6000)
+        cfg = gb.TrainConfig(dim=32, total_epochs=30, negative_samples=3, seed=4,
+                             deterministic=True)
+        ref, _ = gb.train_multilevel_sharded(g, cfg, num_ranks=2)
+        for r in range(2):
+            assert np.array_equal(np.load(f"{out}.{r}.npy"), ref), r
