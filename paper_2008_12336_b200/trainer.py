@@ -369,12 +369,20 @@ def level_bytes(g: Graph, dim: int) -> int:
 
 def train_multilevel(g0: Graph, cfg: TrainConfig, budget=None, threshold: int = 100,
                      no_coarsen: bool = False, hierarchy: Hierarchy | None = None,
-                     return_device: bool = False):
+                     return_device: bool = False, release_levels: bool | None = None):
     """Coarsen, then train from the coarsest level down to g0
     (trainer.py:252-288).  The matrix lives in HBM throughout; levels whose
     footprint exceeds budget.resident_bytes take the partitioned path.
-    Returns numpy float32 [V0, d] (or the CUDA tensor with return_device)."""
+    Returns numpy float32 [V0, d] (or the CUDA tensor with return_device).
+
+    release_levels (default: when the hierarchy is built here): a coarse
+    level's device CSR and mapping are dropped as soon as the next finer
+    matrix is expanded from it, so the finest level's matrix can take the
+    HBM the coarse levels held (C5 at d=256 on one GPU: 116 GB matrix + 34 GB
+    CSR)."""
     cfg.validate()
+    if release_levels is None:
+        release_levels = hierarchy is None
     if hierarchy is None:
         hierarchy = (Hierarchy(graphs=[g0], mappings=[]) if no_coarsen
                      else coarsen_all(g0, threshold=threshold, num_workers=cfg.num_workers))
@@ -394,7 +402,15 @@ def train_multilevel(g0: Graph, cfg: TrainConfig, budget=None, threshold: int = 
                 from .bigtrain import train_large
                 train_large(g_i, M, cfg, e_i, budget, rng_stream=i)
         if i > 0:
-            M = expand_embedding(M, hierarchy.mappings[i - 1])
+            if release_levels:
+                g_i._xadj_dev = g_i._adj_dev = None
+                g_i.__dict__.pop("_active", None)
+                M_next = expand_embedding(M, hierarchy.mappings[i - 1])
+                del M
+                hierarchy.mappings[i - 1]._map_dev = None
+                M = M_next
+            else:
+                M = expand_embedding(M, hierarchy.mappings[i - 1])
     return M if return_device else device_to_numpy(M)
 
 
