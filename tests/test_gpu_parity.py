@@ -804,3 +804,20 @@ def test_host_register_failure_leaves_no_sticky_error(cuda):
         torch.cuda.synchronize()
     finally:
         assert L.gb_host_unregister(a.ctypes.data) == _lib.GB_OK
+
+
+def test_train_multilevel_release_levels_same_result(cuda, orc):
+    """release_levels drops each coarse level's CSR and map once the finer
+    matrix is expanded (the C5-on-one-GPU memory plan) and changes nothing
+    in the result (deterministic kernels)."""
+    x, a = orc.rmat_graph(11, 20000, 4, densify_ids=True)
+    cfg = gb.TrainConfig(dim=32, total_epochs=20, negative_samples=3, seed=2,
+                         deterministic=True)
+    g = Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
+    h1 = gb.coarsen_all(g, threshold=100)
+    ref = gb.train_multilevel(g, cfg, hierarchy=h1)
+    h2 = gb.coarsen_all(g, threshold=100)
+    got = gb.train_multilevel(g, cfg, hierarchy=h2, release_levels=True)
+    assert np.array_equal(got, ref)
+    assert h2.depth > 2 and all(gl._adj_dev is None for gl in h2.graphs[1:])
+    assert h1.graphs[1]._adj_dev is not None  # kept by default for a caller's hierarchy
