@@ -164,6 +164,8 @@ def numpy_to_device(a):
 def copy_device_to_numpy(dst, t) -> None:
     """numpy array dst (C-contiguous) <- CUDA tensor t (same number of bytes)."""
     import numpy as np
+    if not dst.flags.c_contiguous:
+        raise ValueError("copy_device_to_numpy needs a C-contiguous destination")
     t = t.detach().contiguous()
     dst8 = dst.reshape(-1).view(np.uint8)
     if dst8.nbytes < _SMALL or torch.from_numpy(dst8).is_pinned():
