@@ -821,3 +821,46 @@ def test_train_multilevel_release_levels_same_result(cuda, orc):
     assert np.array_equal(got, ref)
     assert h2.depth > 2 and all(gl._adj_dev is None for gl in h2.graphs[1:])
     assert h1.graphs[1]._adj_dev is not None  # kept by default for a caller's hierarchy
+
+
+def _fd_nce_gradient(v, s, b, h=1e-6):
+    """Central differences of the NCE objective b log sig(v.s) + (1-b) log
+    sig(-v.s) (the reference's criterion 7, test_trainer.py:25-42)."""
+    def loss(vv, ss):
+        x = float(np.dot(vv, ss))
+        sig = 1.0 / (1.0 + np.exp(-x))
+        return b * np.log(sig) + (1 - b) * np.log(1.0 - sig)
+    gv = np.array([(loss(v + h * e, s) - loss(v - h * e, s)) / (2 * h) for e in np.eye(len(v))])
+    gs = np.array([(loss(v, s + h * e) - loss(v, s - h * e)) / (2 * h) for e in np.eye(len(s))])
+    return gv, gs
+
+
+@pytest.mark.parametrize("deterministic", [True, False])
+def test_update_matches_finite_difference_gradient(cuda, deterministic):
+    """Every device update is an SGD step on the NCE objective: (new - old) /
+    lr equals its finite-difference gradient within 1e-4 relative (EXACT
+    kernel, and the fast-sigmoid Hogwild kernel on independent pairs)."""
+    rng = np.random.default_rng(2024)
+    n = 300
+    dims = rng.integers(2, 9, size=n)
+    worst = 0.0
+    for d in sorted(set(dims.tolist())):
+        idx = np.nonzero(dims == d)[0]
+        m = idx.shape[0]
+        M = (rng.random((2 * m, d)) - 0.5).astype(np.float32)
+        b = rng.integers(0, 2, size=m)
+        before = M.astype(np.float64)
+        # pair i: source 2i, sample 2i+1; one list entry per source
+        for lab in (0, 1):
+            sel = np.nonzero(b == lab)[0]
+            if sel.size == 0:
+                continue
+            gb.apply_sample_lists(M, 2 * sel, (2 * sel + 1)[:, None], [lab], 0.25,
+                                  deterministic=deterministic)
+        for i in range(m):
+            gv, gs = _fd_nce_gradient(before[2 * i], before[2 * i + 1], int(b[i]))
+            dv = (M[2 * i].astype(np.float64) - before[2 * i]) / 0.25
+            ds = (M[2 * i + 1].astype(np.float64) - before[2 * i + 1]) / 0.25
+            num = np.linalg.norm(np.concatenate([dv, ds]) - np.concatenate([gv, gs]))
+            worst = max(worst, num / np.linalg.norm(np.concatenate([gv, gs])))
+    assert worst <= 1e-4, worst
