@@ -1053,10 +1053,14 @@ def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
                 M = store.to_full(group=group, distributed=distributed)
                 store = None
             M = expand_embedding(M, mapping)
+    clear_rotation_graphs()  # the cached rotation holds pool buffers and the CSR
     if store is not None:
         if return_parts:
             return store, stats
         M = store.to_full(group=group, distributed=distributed)
     elif distributed and not broadcast_done:
         _broadcast(M, group)
-    return (M if return_device else M.cpu().numpy()), stats
+    if return_device:
+        return M, stats
+    from ._staging import device_to_numpy
+    return device_to_numpy(M), stats
