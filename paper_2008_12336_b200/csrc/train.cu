@@ -91,9 +91,30 @@ bool use_hot(unsigned flags) {
          (flags & GB_TRAIN_ATOMIC) && !(flags & GB_TRAIN_REUSE);
 }
 
+// The default flags except the fast sigmoid: the fp64-sigmoid KIND 3 pass.
+bool use_hot_f64(unsigned flags) {
+  static const bool off = [] {
+    const char *e = std::getenv("GB_NO_HOT");
+    return e && std::atoi(e) != 0;
+  }();
+  return !off && !(flags & GB_TRAIN_EXACT) && !(flags & GB_TRAIN_FAST_SIGMOID) &&
+         (flags & GB_TRAIN_ATOMIC) && !(flags & GB_TRAIN_REUSE);
+}
+
 void select_hot(Variant &v, unsigned flags, bool diagonal, bool pool_materialized = true,
                 bool pool_balanced = false) {
-  if (!use_hot(flags)) return;
+  if (!use_hot(flags)) {
+    if (!use_hot_f64(flags)) return;
+    // the same compile-time flags with the reference's fp64 sigmoid
+    v.pass_hot = v.pass_hot_f64;
+    v.pass_ahead_hot = v.pass_ahead_hot_f64;
+    v.pass_pipe_hot = v.pass_pipe_hot_f64;
+    v.pool_hot = v.pool_hot_f64;
+    v.pool_hot_diag = v.pool_hot_diag_f64;
+    v.pool_bal_hot = v.pool_bal_hot_f64;
+    v.pool_bal_hot_diag = v.pool_bal_hot_diag_f64;
+    v.pass_staged_hot = v.pass_staged_hot_f64;
+  }
   // GB_PASS_AHEAD=1: the KIND 2 throughput pass (index chain one source
   // ahead): +1.3% on C2 but -8% / -10% on C3's second and third levels
   // (high-degree, partly L2-resident), so the inline chain is the default
@@ -195,10 +216,14 @@ static int train_passes_impl(int64_t num_vertices, const int64_t *xadj, const in
       const int64_t want = std::min<int64_t>(max_groups > 0 ? max_groups : INT64_MAX, items);
       const char *env = std::getenv("GB_PASS_SMEM");
       const bool on = env ? std::atoi(env) != 0 : want >= full0;
-      if (on && var.pass_staged_hot && use_hot(flags) && !ppr) var.pass = var.pass_staged_hot;
+      // (select_hot swapped in the fp64-sigmoid instantiations without
+      // GB_TRAIN_FAST_SIGMOID)
+      if (on && var.pass_staged_hot && (use_hot(flags) || use_hot_f64(flags)) && !ppr)
+        var.pass = var.pass_staged_hot;
       fn = var.pass;
     }
-    if (var.pass_staged_hot && var.pass == var.pass_staged_hot) {
+    const bool staged = var.pass && var.pass == var.pass_staged_hot;
+    if (staged) {
       smem = (size_t)(kBlock / var.G) * kChunk * dim * sizeof(float);
       GB_CUDA_TRY(cudaFuncSetAttribute((const void *)var.pass,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

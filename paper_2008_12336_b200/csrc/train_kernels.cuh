@@ -748,11 +748,11 @@ __device__ __forceinline__ SourceIdx shfl_source(const SourceIdx &d, int k, unsi
 }
 
 // Row half of a source: gather, chained updates, write-back.
-template <class Row, bool EXACT, bool BATCH, bool HOT>
+template <class Row, bool EXACT, bool BATCH, bool HOT, bool F64S = false>
 __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &g,
                                              const SourceIdx &d, bool &bad, int &first_bad) {
   const int nsamp = 1 + a.n_neg;
-  const bool fast = HOT || a.fast, atomic = HOT || a.atomic, reuse = !HOT && a.reuse;
+  const bool fast = HOT ? !F64S : a.fast, atomic = HOT || a.atomic, reuse = !HOT && a.reuse;
   const double lr = (double)d.lr;
   Row S;
   S.load(a.M + (int64_t)d.v * a.dim, g.gl, a.dim);
@@ -797,7 +797,9 @@ __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &
 // sigmoid, vector-reduction write-back, no reuse) fixed at compile time --
 // the runtime-flag branches otherwise triple the unrolled code, and the
 // i-cache misses that cost show up as the top ncu stall (no_instructions).
-template <class Row, bool EXACT, int KIND, bool HOT>
+// F64S (with HOT): the same compile-time flags but the reference's fp64
+// sigmoid and divide (trainer.py:118) instead of the fp32 one.
+template <class Row, bool EXACT, int KIND, bool HOT, bool F64S = false>
 __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 ? 3 : Row::kMinBlocks))
     train_passes_kernel(PassArgs a) {
   constexpr int G = Row::G;
@@ -805,7 +807,7 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 
   // KIND 0 / 2 keep the source's initial copy in a shared slot per group
   // (launched with kBlock / G * dim floats of dynamic shared memory)
   constexpr bool kS0Smem = Row::kStageable && !EXACT;
-  const bool fast = HOT || a.fast, atomic = HOT || a.atomic, reuse = !HOT && a.reuse;
+  const bool fast = HOT ? !F64S : a.fast, atomic = HOT || a.atomic, reuse = !HOT && a.reuse;
   const GroupCtx g = group_ctx<Row>();
   const Slots<Row> sl(a.max_groups);
   if (sl.warp_idle()) return;
@@ -1008,7 +1010,7 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 
 #pragma unroll 1
       for (int k = 0; k < kmax; ++k) {
         const SourceIdx d = shfl_source(mine, k, g.gmask, G);
-        if (d.active) train_source<Row, EXACT, BATCH, HOT>(a, g, d, bad, first_bad);
+        if (d.active) train_source<Row, EXACT, BATCH, HOT, F64S>(a, g, d, bad, first_bad);
       }
     }
   }
@@ -1096,7 +1098,7 @@ __device__ __forceinline__ int64_t lower_bound_adj(const int32_t *__restrict__ a
 // flat samples l, l + G, ... of the window (the positive from the pool or the
 // CSR, a negative from the counter-based key), and the chunks take them by
 // shuffle -- the RNG runs once per sample instead of once per lane.
-template <class Row, bool EXACT, int MODE>
+template <class Row, bool EXACT, int MODE, bool F64S = false>
 __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_pool_kernel(PoolArgs a) {
   constexpr int G = Row::G;
   constexpr int kWin = 2 * kChunk;
@@ -1109,7 +1111,7 @@ __global__ void __launch_bounds__(kBlock, EXACT ? 1 : Row::kMinBlocks) train_poo
   if (sl.warp_idle()) return;
   constexpr bool HOT = MODE != 0;
   constexpr bool BALC = MODE >= 3;  // HOT on balanced pools
-  const bool fast = HOT || a.fast, atomic = HOT || a.atomic, reuse = !HOT && a.reuse;
+  const bool fast = HOT ? !F64S : a.fast, atomic = HOT || a.atomic, reuse = !HOT && a.reuse;
   const bool diagonal = HOT ? (MODE == 2 || MODE == 4) : a.Msrc == a.Mtgt;
   const bool bal = BALC || (!HOT && a.bal_npos != nullptr);
   const int per_t = 1 + a.n_neg;
@@ -1313,6 +1315,14 @@ struct Variant {
   PassFn pass_hot = nullptr;
   PassFn pass_ahead_hot = nullptr;  // KIND 2
   PassFn pass_staged_hot = nullptr;  // KIND 3
+  PassFn pass_staged_hot_f64 = nullptr;  // KIND 3 with the fp64 sigmoid
+  PassFn pass_hot_f64 = nullptr;
+  PassFn pass_ahead_hot_f64 = nullptr;
+  PassFn pass_pipe_hot_f64 = nullptr;
+  PoolFn pool_hot_f64 = nullptr;
+  PoolFn pool_hot_diag_f64 = nullptr;
+  PoolFn pool_bal_hot_f64 = nullptr;
+  PoolFn pool_bal_hot_diag_f64 = nullptr;
   PassFn pass_pipe_hot = nullptr;
   PoolFn pool_hot = nullptr;       // off-diagonal pair
   PoolFn pool_hot_diag = nullptr;  // diagonal pair (Msrc == Mtgt)
@@ -1333,6 +1343,14 @@ Variant make_variant() {
     v.pass_hot = train_passes_kernel<Row, false, 0, true>;
     v.pass_ahead_hot = train_passes_kernel<Row, false, 2, true>;
     v.pass_staged_hot = train_passes_kernel<Row, false, 3, true>;
+    v.pass_staged_hot_f64 = train_passes_kernel<Row, false, 3, true, true>;
+    v.pass_hot_f64 = train_passes_kernel<Row, false, 0, true, true>;
+    v.pass_ahead_hot_f64 = train_passes_kernel<Row, false, 2, true, true>;
+    v.pass_pipe_hot_f64 = train_passes_kernel<Row, false, 1, true, true>;
+    v.pool_hot_f64 = train_pool_kernel<Row, false, 1, true>;
+    v.pool_hot_diag_f64 = train_pool_kernel<Row, false, 2, true>;
+    v.pool_bal_hot_f64 = train_pool_kernel<Row, false, 3, true>;
+    v.pool_bal_hot_diag_f64 = train_pool_kernel<Row, false, 4, true>;
     v.pass_pipe_hot = train_passes_kernel<Row, false, 1, true>;
     v.pool_hot = train_pool_kernel<Row, false, 1>;
     v.pool_hot_diag = train_pool_kernel<Row, false, 2>;

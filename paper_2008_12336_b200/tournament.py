@@ -48,7 +48,7 @@ from . import _lib
 from .bigtrain import PairSides, PartitionPlan, _derived_seed, rotation_pairs
 from .errors import ConfigError, PlanError
 from .graph import Graph
-from .trainer import TrainConfig, lr_at
+from .trainer import TrainConfig, _train_flags, lr_at
 
 TOP, BOT = 0, 1
 
@@ -155,9 +155,7 @@ class DevicePair:
     def __init__(self, g: Graph, cfg: TrainConfig, B: int, K: int = 1,
                  status: torch.Tensor | None = None):
         _lib.require_cuda()
-        flags = (_lib.GB_TRAIN_REUSE if cfg.reuse_updated_source else 0) | (
-            _lib.GB_TRAIN_EXACT if cfg.deterministic else _lib.GB_TRAIN_FAST_SIGMOID) | (
-            _lib.GB_TRAIN_ATOMIC if cfg.atomic_rows and not cfg.deterministic else 0)
+        flags = _train_flags(cfg, pair=True)
         self.status = status if status is not None else _lib.new_status()
         self.sides = PairSides(g.device_csr(), cfg, flags, B, self.status, K=K)
 

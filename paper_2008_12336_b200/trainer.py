@@ -42,6 +42,8 @@ SIGMOID_CLAMP = 10.0
 LR_FLOOR = 1e-4
 EPOCH_UNITS = ("vertex-pass", "edge-scaled")
 SIMILARITIES = ("adjacency", "ppr")
+# GB_FAST_SIGMOID=0/1 overrides TrainConfig.fast_sigmoid's default (A/B runs)
+FAST_SIGMOID_DEFAULT = {"0": False, "1": True}.get(os.environ.get("GB_FAST_SIGMOID", ""))
 # auto in-flight policy max(FLOOR, V / DIVISOR).  Default: uncapped (the
 # cap is >= V).  Round 1 needed max(256, V/16) to hold C1 AUCROC to the
 # reference while source rows were written back with plain stores; with the
@@ -78,6 +80,12 @@ class TrainConfig:
     # in-memory levels only: the part-pair pools are adjacency by design)
     similarity: str = "adjacency"
     ppr_alpha: float = 0.85
+    # parallel kernels' sigmoid: False = fp64 like the reference
+    # (trainer.py:118), True = fp32 cancellation-free form (~1e-7 relative),
+    # None = auto: fp64 in the vertex passes (no cost: 5.44 vs 5.44 G upd/s
+    # on C2), fp32 in the part-pair kernels (6% faster at K=2;
+    # profiles/r02_sigmoid_fp64_vs_fp32.jsonl)
+    fast_sigmoid: bool | None = FAST_SIGMOID_DEFAULT
 
     def validate(self) -> None:
         if self.dim < 1:
@@ -179,11 +187,17 @@ class _DeviceMatrix:
             torch.cuda.current_stream().synchronize()
 
 
-def _train_flags(cfg: TrainConfig) -> int:
+def _train_flags(cfg: TrainConfig, pair: bool = False) -> int:
     """EXACT kernels when deterministic; otherwise the parallel kernels with
-    the fp32 cancellation-free sigmoid (fp64 dot kept)."""
+    the reference's fp64 sigmoid or the fp32 cancellation-free one
+    (TrainConfig.fast_sigmoid; auto: fp64 for passes, fp32 for pair
+    kernels), fp64 dot either way."""
     flags = _lib.GB_TRAIN_REUSE if cfg.reuse_updated_source else 0
-    flags |= _lib.GB_TRAIN_EXACT if cfg.deterministic else _lib.GB_TRAIN_FAST_SIGMOID
+    fast = pair if cfg.fast_sigmoid is None else cfg.fast_sigmoid
+    if cfg.deterministic:
+        flags |= _lib.GB_TRAIN_EXACT
+    elif fast:
+        flags |= _lib.GB_TRAIN_FAST_SIGMOID
     if cfg.atomic_rows and not cfg.deterministic:
         flags |= _lib.GB_TRAIN_ATOMIC
     return flags

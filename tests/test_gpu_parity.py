@@ -290,7 +290,7 @@ def test_atomic_rows_keep_concurrent_updates_of_a_hot_row(cuda, orc):
     assert _rel_err(Ma[others], ref[others]) <= 1e-4
 
 
-@pytest.mark.parametrize("variant", ["throughput", "latency", "staged"])
+@pytest.mark.parametrize("variant", ["throughput", "latency", "staged", "staged_f64"])
 @pytest.mark.parametrize("d", [16, 32, 64, 128, 256])
 def test_single_group_passes_match_sequential(cuda, orc, d, variant, monkeypatch):
     """The parallel pass kernels (throughput, latency and shared-memory-staged
@@ -298,14 +298,15 @@ def test_single_group_passes_match_sequential(cuda, orc, d, variant, monkeypatch
     up to the tree dot and fp32 sigmoid: within 1e-5 relative after two
     passes."""
     monkeypatch.setenv("GB_PIPE", "1" if variant == "latency" else "0")
-    monkeypatch.setenv("GB_PASS_SMEM", "1" if variant == "staged" else "0")
+    monkeypatch.setenv("GB_PASS_SMEM", "1" if variant.startswith("staged") else "0")
     x, a = orc.rmat_graph(11, 20000, 3, densify_ids=True)
     g = Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
     M0 = orc.init_embedding(g.num_vertices, d, 1) * 20.0
     ref = M0.copy()
     orc.train_level(x, a, ref, d, 2, 0.035, 3, 1, 0)
     M = M0.copy()
-    gb.train_level(g, M, gb.TrainConfig(dim=d, max_inflight=1), 2)
+    cfg = gb.TrainConfig(dim=d, max_inflight=1, fast_sigmoid=variant != "staged_f64")
+    gb.train_level(g, M, cfg, 2)
     assert _rel_err(M, ref) <= REL_TOL
 
 
