@@ -3,9 +3,11 @@
 numpy/ctypes front end of ``oracle/gosh_oracle.c``, a plain-C restatement of
 the reference's numba kernels (``/root/reference/pkg/src/mlembed``; each
 function cites the file:line it follows).  Only ``tests/``,
-``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline legs may import
-this module, and only as the checker -- never as the thing measured or
-shipped.  The product package (``paper_2008_12336_b200``) never imports it.
+``__graft_entry__.smoke()``, ``bench.py``'s CPU-baseline legs and the
+measurement scripts' CPU-baseline / reference legs (``scripts/``) import
+this module, and only as the checker or the CPU reference -- never as the
+GPU side measured or shipped.  The product package (``paper_2008_12336_b200``)
+never imports it (``tests/test_host_cpu.py`` enforces that).
 
 Pinning: ``tests/test_oracle_golden.py`` checks every function here against
 golden vectors produced by the reference itself
