@@ -150,6 +150,30 @@ def test_c1_aucroc_parity_with_reference(cuda):
     assert abs(np.mean(mine) - np.mean([runs[s] for s in seeds])) <= AUC_TOL, msg
 
 
+def test_c1_sharded_aucroc_parity_with_reference(cuda):
+    """The multi-GPU path (train_multilevel_sharded: balanced pools, two
+    sharded levels, here 2 virtual ranks = K=4 parts) on the same C1
+    protocol, paired with the reference's seeds: the north star's AUCROC bar
+    holds for the sharded path too (30 seeds at 2/4/8 ranks: +0.0019 /
+    +0.0048 / +0.0044, profiles/r02_c1_sharded_aucroc_parity.jsonl)."""
+    ref, pr, setup = _c1_setup()
+    runs = {r["seed"]: r["aucroc"] for r in ref["runs"]}
+    seeds = sorted(runs)[:24]
+    mine = []
+    for seed in seeds:
+        cfg = gb.TrainConfig(dim=pr["dim"], total_epochs=pr["total_epochs"],
+                             smoothing_ratio=pr["smoothing_ratio"],
+                             learning_rate=pr["learning_rate"],
+                             negative_samples=pr["negative_samples"], seed=seed,
+                             epoch_unit=pr["epoch_unit"])
+        M, _ = gb.train_multilevel_sharded(setup.train_graph, cfg, hierarchy=setup.hierarchy,
+                                           num_ranks=2, return_device=True)
+        mine.append(setup.score(M))
+    ci = aucroc_parity_interval(np.array(mine) - np.array([runs[s] for s in seeds]))
+    assert abs(ci["mean"]) <= AUC_TOL, ci
+    assert -AUC_TOL <= ci["lo"] and ci["hi"] <= AUC_TOL, ci
+
+
 # -- row-block (chunked) graph construction: the C5 path -----------------------------
 @pytest.mark.parametrize("dens", [False, True])
 def test_blocked_rmat_csr_equals_one_shot(cuda, dens):
