@@ -442,10 +442,12 @@ int gb_csr_validate(int64_t num_vertices, int64_t num_edges, const int64_t *xadj
  * lines end at '\n'; blank and '#' lines are skipped; a line must hold two
  * fields that Python's int() accepts ([+-]?digits with single underscores
  * between digits).  u_out/v_out (room for num_bytes/2+1 entries) receive the
- * ids of the edge lines in order.  result (host, 4 x int64): edges, lines,
+ * ids of the edge lines in order.  result (host, 5 x int64): edges, lines,
  * index of the first malformed line (-1 if none), 1 if a syntactically valid
- * id lies outside int64 (the reference's later OverflowError).  ASCII text
- * only (the caller routes other text to the host parser).  Synchronizes. */
+ * id lies outside int64 (the reference's later OverflowError), 1 if the text
+ * holds a byte >= 0x80 or a '\r' not followed by '\n' -- text whose lines
+ * or fields Python splits differently, which the caller hands to the host
+ * parser (the other results are then not meaningful).  Synchronizes. */
 int gb_parse_edge_text_workspace(int64_t num_bytes, size_t *bytes);
 int gb_parse_edge_text(const char *text, int64_t num_bytes, int64_t *u_out, int64_t *v_out,
                        int64_t *result, void *workspace, size_t ws_bytes,

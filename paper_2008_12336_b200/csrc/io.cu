@@ -117,9 +117,18 @@ __device__ int parse_int(const unsigned char *s, int64_t n, int64_t *out) {
   return 0;
 }
 
+// Also flags text the host must parse: a byte >= 0x80 (int() accepts
+// non-ASCII digits and str.split non-ASCII spaces) or a '\r' not followed by
+// '\n' (a line break under universal newlines).
 __global__ void line_start_flags(const unsigned char *__restrict__ text, int64_t n,
-                                 uint8_t *__restrict__ flag) {
-  STRIDE(p, n) flag[p] = (p == 0 || text[p - 1] == '\n') ? 1 : 0;
+                                 uint8_t *__restrict__ flag, int *__restrict__ needs_host) {
+  int h = 0;
+  STRIDE(p, n) {
+    const unsigned char c = text[p];
+    flag[p] = (p == 0 || text[p - 1] == '\n') ? 1 : 0;
+    if (c >= 0x80 || (c == '\r' && (p + 1 >= n || text[p + 1] != '\n'))) h = 1;
+  }
+  if (h) atomicOr(needs_host, 1);
 }
 
 __global__ void parse_lines(const unsigned char *__restrict__ text, int64_t n,
@@ -196,6 +205,7 @@ struct TextLayout {
   uint8_t *ok;
   unsigned long long *first_bad;
   int *overflow;
+  int *needs_host;
   void *tmp;
   size_t tmp_bytes;
 };
@@ -209,6 +219,7 @@ int text_layout(Carve &c, int64_t n, TextLayout &t) {
   t.nsel = c.take<int64_t>(1);
   t.first_bad = c.take<unsigned long long>(1);
   t.overflow = c.take<int>(1);
+  t.needs_host = c.take<int>(1);
   size_t a = 0, b = 0;
   thrust::counting_iterator<int64_t> it(0);
   GB_CUDA_TRY(cub::DeviceSelect::Flagged(nullptr, a, it, (uint8_t *)nullptr, (int64_t *)nullptr,
@@ -277,7 +288,8 @@ GB_API int gb_parse_edge_text(const char *text, int64_t num_bytes, int64_t *u_ou
   if (rc) return rc;
   GB_REQUIRE(c.off <= ws_bytes, "gb_parse_edge_text: workspace too small");
   const unsigned char *s = reinterpret_cast<const unsigned char *>(text);
-  line_start_flags<<<grid_for(num_bytes), 256, 0, st>>>(s, num_bytes, t.flag);
+  GB_CUDA_TRY(cudaMemsetAsync(t.needs_host, 0, sizeof(int), st));
+  line_start_flags<<<grid_for(num_bytes), 256, 0, st>>>(s, num_bytes, t.flag, t.needs_host);
   GB_CHECK_LAUNCH();
   thrust::counting_iterator<int64_t> it(0);
   size_t tb = t.tmp_bytes;
@@ -296,15 +308,17 @@ GB_API int gb_parse_edge_text(const char *text, int64_t num_bytes, int64_t *u_ou
   GB_CUDA_TRY(cub::DeviceSelect::Flagged(t.tmp, tb, t.V, t.ok, v_out, t.nsel, L, st));
   int64_t m = 0;
   unsigned long long bad = 0;
-  int over = 0;
+  int over = 0, host = 0;
   GB_CUDA_TRY(cudaMemcpyAsync(&m, t.nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GB_CUDA_TRY(cudaMemcpyAsync(&bad, t.first_bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
   GB_CUDA_TRY(cudaMemcpyAsync(&over, t.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GB_CUDA_TRY(cudaMemcpyAsync(&host, t.needs_host, sizeof(int), cudaMemcpyDeviceToHost, st));
   GB_CUDA_TRY(cudaStreamSynchronize(st));
   result[0] = m;
   result[1] = L;
   result[2] = bad == ~0ull ? -1 : (int64_t)bad;
   result[3] = over;
+  result[4] = host;
   return GB_OK;
 }
 

@@ -363,7 +363,130 @@ def _edges_to_graph(src: torch.Tensor, dst: torch.Tensor, directed: bool) -> Gra
     return _csr_device(int(k.value), ids[:m], ids[m:], flags, directed, orig_ids=orig)
 
 
-EDGE_TEXT_CHUNK = 256 << 20  # characters per device parse
+EDGE_TEXT_CHUNK = 256 << 20  # characters (bytes) per device parse
+
+
+class _NeedsText(Exception):
+    """The byte fast path met text Python splits differently (non-ASCII, a
+    lone carriage return): restart on the text stream."""
+
+
+class _EdgeTextParser:
+    """Device parse of newline-terminated ASCII chunks (gb_parse_edge_text),
+    accumulating the edge ids; malformed lines are re-read by the host loop
+    for the reference's message."""
+
+    def __init__(self):
+        self.parts_u: list[torch.Tensor] = []
+        self.parts_v: list[torch.Tensor] = []
+        self.line_base = 0
+        self.overflow = False
+        self.ws, self.wsb = None, 0
+        self.text = None
+
+    def host_chunk(self, body: str) -> None:
+        lines = body.split("\n")
+        if body.endswith("\n"):
+            lines.pop()
+        us, vs = _parse_edge_lines_host(lines, self.line_base)
+        if any(not -2**63 <= x < 2**63 for x in us + vs):
+            self.overflow = True
+        elif us:
+            self.parts_u.append(torch.tensor(us, dtype=torch.int64))
+            self.parts_v.append(torch.tensor(vs, dtype=torch.int64))
+        self.line_base += len(lines)
+
+    def device_chunk(self, pieces, body_text) -> bool:
+        """pieces: numpy uint8 arrays whose concatenation is the chunk.
+        Returns False (nothing consumed) when the chunk needs the host."""
+        from ._staging import copy_numpy_to_device
+        n = sum(int(p.shape[0]) for p in pieces)
+        if self.text is None or self.text.numel() < n:
+            self.text = torch.empty(max(n, 1), dtype=torch.uint8, device="cuda")
+        off = 0
+        for p in pieces:
+            if p.shape[0]:
+                copy_numpy_to_device(self.text[off:off + p.shape[0]], p)
+                off += p.shape[0]
+        need = C.c_size_t(0)
+        _lib.call("gb_parse_edge_text_workspace", n, C.byref(need))
+        if self.ws is None or self.wsb < need.value:
+            self.ws = None
+            self.ws, self.wsb = _lib.workspace("gb_parse_edge_text_workspace", n)
+        cap = n // 2 + 1
+        du = torch.empty(cap, dtype=torch.int64, device="cuda")
+        dv = torch.empty(cap, dtype=torch.int64, device="cuda")
+        res = (C.c_int64 * 5)()
+        _lib.call("gb_parse_edge_text", _lib.ptr(self.text), n, _lib.ptr(du), _lib.ptr(dv), res,
+                  _lib.ptr(self.ws), self.wsb, _lib.stream())
+        m, L, bad, over, host = (int(x) for x in res)
+        if host:
+            return False
+        if bad >= 0:
+            body = body_text()
+            lines = body.split("\n")
+            _parse_edge_lines_host(lines[bad:bad + 1], self.line_base + bad)
+            # the device flagged a line the host accepts: trust the host
+            us, vs = _parse_edge_lines_host(lines[:-1] if body.endswith("\n") else lines,
+                                            self.line_base)
+            du = torch.tensor(us, dtype=torch.int64, device="cuda")
+            dv = torch.tensor(vs, dtype=torch.int64, device="cuda")
+            m = len(us)
+        self.overflow = self.overflow or bool(over)
+        self.parts_u.append(du[:m])
+        self.parts_v.append(dv[:m])
+        self.line_base += L
+        return True
+
+    def graph(self, directed: bool) -> Graph:
+        self.ws = self.text = None
+        if self.overflow:
+            raise OverflowError("Python int too large to convert to C long")
+        if sum(int(t.numel()) for t in self.parts_u) == 0:
+            raise EmptyGraphError("edge list contains no edges")
+        src = torch.cat([t.cuda() for t in self.parts_u])
+        dst = torch.cat([t.cuda() for t in self.parts_v])
+        return _edges_to_graph(src, dst, directed)
+
+
+def _byte_source(text_stream):
+    """The binary file under a fresh TextIOWrapper with an ASCII-compatible
+    encoding, else None."""
+    import codecs
+    raw = getattr(text_stream, "buffer", None)
+    enc = getattr(text_stream, "encoding", None)
+    try:
+        if raw is None or enc is None or not raw.seekable() or text_stream.tell() != 0:
+            return None
+        name = codecs.lookup(enc).name
+    except (OSError, LookupError, ValueError):
+        return None
+    return raw if name in ("utf-8", "ascii", "latin-1", "iso8859-1", "cp1252") else None
+
+
+def _parse_bytes(raw, parser: _EdgeTextParser) -> None:
+    """Chunks of the binary file, cut after their last newline."""
+    carry = b""
+    while True:
+        s = raw.read(EDGE_TEXT_CHUNK)
+        eof = not s
+        if not eof:
+            cut = s.rfind(b"\n")
+            if cut < 0:
+                carry += s
+                continue
+            pieces = [np.frombuffer(carry, np.uint8), np.frombuffer(s, np.uint8, count=cut + 1)]
+            tail = s[cut + 1:]
+        else:
+            pieces, tail = [np.frombuffer(carry, np.uint8)], b""
+        if sum(p.shape[0] for p in pieces):
+            body = (lambda c=carry, s_=s, k=(cut + 1 if not eof else 0):
+                    (c + s_[:k]).decode("ascii"))
+            if not parser.device_chunk(pieces, body):
+                raise _NeedsText()
+        carry = tail
+        if eof:
+            break
 
 
 def load_edge_list(text_stream: IO[str], directed: bool = False) -> Graph:
@@ -376,8 +499,12 @@ def load_edge_list(text_stream: IO[str], directed: bool = False) -> Graph:
     there (gb_unique_ids) before the CSR build; errors are the reference's
     (the first malformed line is re-read by the host loop for its message;
     a valid id outside int64 raises OverflowError after the whole input, as
-    numpy's conversion does).  Non-ASCII chunks go through the host loop.
-    Without a GPU the host loop parses everything (the CSR still needs one)."""
+    numpy's conversion does).  A text file opened with an ASCII-compatible
+    encoding is read as bytes straight from its buffer (no decode/encode);
+    text the host splits differently (non-ASCII, lone carriage returns)
+    goes through the host loop -- for a file, from the start on the text
+    stream, for other streams chunk by chunk.  Without a GPU the host loop
+    parses everything (the CSR still needs one)."""
     if not torch.cuda.is_available():
         us, vs = _parse_edge_lines_host(text_stream)
         if not us:
@@ -386,15 +513,20 @@ def load_edge_list(text_stream: IO[str], directed: bool = False) -> Graph:
         v_arr = np.asarray(vs, dtype=np.int64)
         return _edges_to_graph(torch.from_numpy(u_arr), torch.from_numpy(v_arr), directed)
     _lib.require_cuda()
-    parts_u: list[torch.Tensor] = []
-    parts_v: list[torch.Tensor] = []
-    line_base, overflow, carry = 0, False, ""
-    ws = None
-    wsb = 0
+    raw = _byte_source(text_stream)
+    if raw is not None:
+        parser = _EdgeTextParser()
+        try:
+            _parse_bytes(raw, parser)
+            return parser.graph(directed)
+        except _NeedsText:
+            text_stream.seek(0)
+    parser = _EdgeTextParser()
+    carry = ""
     while True:
         s = text_stream.read(EDGE_TEXT_CHUNK)
         eof = not s
-        buf = carry + s
+        buf = carry + s if carry else s
         if not eof:
             cut = buf.rfind("\n")
             if cut < 0:
@@ -404,57 +536,12 @@ def load_edge_list(text_stream: IO[str], directed: bool = False) -> Graph:
         else:
             body, carry = buf, ""
         if body:
-            if not body.isascii():
-                lines = body.split("\n")
-                if body.endswith("\n"):
-                    lines.pop()
-                us, vs = _parse_edge_lines_host(lines, line_base)
-                if any(not -2**63 <= x < 2**63 for x in us + vs):
-                    overflow = True
-                elif us:
-                    parts_u.append(torch.tensor(us, dtype=torch.int64))
-                    parts_v.append(torch.tensor(vs, dtype=torch.int64))
-                line_base += len(lines)
-            else:
-                raw = body.encode("ascii")
-                n = len(raw)
-                text = torch.frombuffer(bytearray(raw), dtype=torch.uint8).cuda()
-                need = C.c_size_t(0)
-                _lib.call("gb_parse_edge_text_workspace", n, C.byref(need))
-                if ws is None or wsb < need.value:
-                    ws = None
-                    ws, wsb = _lib.workspace("gb_parse_edge_text_workspace", n)
-                cap = n // 2 + 1
-                du = torch.empty(cap, dtype=torch.int64, device="cuda")
-                dv = torch.empty(cap, dtype=torch.int64, device="cuda")
-                res = (C.c_int64 * 4)()
-                _lib.call("gb_parse_edge_text", _lib.ptr(text), n, _lib.ptr(du), _lib.ptr(dv),
-                          res, _lib.ptr(ws), wsb, _lib.stream())
-                m, L, bad, over = (int(x) for x in res)
-                if bad >= 0:
-                    lines = body.split("\n")
-                    _parse_edge_lines_host(lines[bad:bad + 1], line_base + bad)
-                    # the device flagged a line the host accepts: trust the host
-                    us, vs = _parse_edge_lines_host(
-                        lines[:-1] if body.endswith("\n") else lines, line_base)
-                    du = torch.tensor(us, dtype=torch.int64, device="cuda")
-                    dv = torch.tensor(vs, dtype=torch.int64, device="cuda")
-                    m = len(us)
-                overflow = overflow or bool(over)
-                parts_u.append(du[:m])
-                parts_v.append(dv[:m])
-                line_base += L
+            enc = body.encode("utf-8")
+            if not parser.device_chunk([np.frombuffer(enc, np.uint8)], lambda b=body: b):
+                parser.host_chunk(body)
         if eof:
             break
-    ws = None
-    if overflow:
-        raise OverflowError("Python int too large to convert to C long")
-    m = sum(int(t.numel()) for t in parts_u)
-    if m == 0:
-        raise EmptyGraphError("edge list contains no edges")
-    src = torch.cat([t.cuda() for t in parts_u])
-    dst = torch.cat([t.cuda() for t in parts_v])
-    return _edges_to_graph(src, dst, directed)
+    return parser.graph(directed)
 
 
 def write_edge_list(g: Graph, text_stream: IO[str]) -> None:

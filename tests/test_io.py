@@ -173,3 +173,40 @@ def test_staged_array_transfers_round_trip(cuda, monkeypatch):
         assert np.array_equal(d.cpu().numpy(), a)
         back = _staging.device_to_numpy(d)
         assert back.dtype == a.dtype and np.array_equal(back, a)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("chunk", [None, 777])
+def test_device_edge_list_from_files(cuda, golden, tmp_path, monkeypatch, chunk):
+    """Text files take the byte fast path (read from the file's buffer, no
+    decode): the golden texts written with LF and CRLF line ends give the
+    reference's graphs and errors; a lone carriage return (a line break under
+    universal newlines) or a non-ASCII byte restarts on the text stream."""
+    if chunk:
+        monkeypatch.setattr(gmod, "EDGE_TEXT_CHUNK", chunk)
+    g = golden("edgelist.npz")
+    for k, (text, directed, xadj, adj, orig) in enumerate(_texts(g)):
+        for nl in ("\n", "\r\n"):
+            p = tmp_path / f"t{k}.txt"
+            p.write_bytes(text.replace("\n", nl).encode("ascii"))
+            with open(p) as f:
+                h = gb.load_edge_list(f, directed=directed)
+            assert np.array_equal(h.xadj, xadj) and np.array_equal(h.adj, adj), (k, nl)
+            assert np.array_equal(h.orig_ids, orig)
+    for e, (text, kind, line, msg) in enumerate(_errors(g)):
+        p = tmp_path / f"e{e}.txt"
+        p.write_bytes(text.encode("utf-8"))
+        with open(p, encoding="utf-8") as f:
+            if kind == "parse":
+                with pytest.raises(EdgeListParseError) as ei:
+                    gb.load_edge_list(f)
+                assert ei.value.line_number == line and str(ei.value) == msg
+            else:
+                with pytest.raises(OverflowError):
+                    gb.load_edge_list(f)
+    # lone CR: Python's text mode splits the line there
+    p = tmp_path / "cr.txt"
+    p.write_bytes(b"# c\n1 2\r3 4\n5 6\n")
+    with open(p) as f:
+        h = gb.load_edge_list(f)
+    assert np.array_equal(h.orig_ids, [1, 2, 3, 4, 5, 6]) and h.num_edges == 6
