@@ -119,9 +119,13 @@ def _par_copy(dst, src) -> None:
 
 def copy_numpy_to_device(dst, a) -> None:
     """dst (contiguous CUDA tensor) <- numpy array a (same number of bytes)."""
+    import warnings
+
     import numpy as np
     a = np.ascontiguousarray(a)
-    t = torch.from_numpy(a)
+    with warnings.catch_warnings():  # read-only views (np.frombuffer): only read here
+        warnings.simplefilter("ignore", UserWarning)
+        t = torch.from_numpy(a)
     if a.nbytes < _SMALL or t.is_pinned():  # page-locked already: one direct DMA
         dst.view(-1).view(torch.uint8).copy_(t.reshape(-1).view(torch.uint8))
         return

@@ -30,6 +30,8 @@ N_LINES = int(os.environ.get("N_LINES", "20000000"))
 
 
 def main():
+    if os.environ.get("SKIP_GSHG"):
+        return text_bench()
     g = gb.rmat_graph(SCALE, SAMPLES, 7, densify_ids=True)
     nbytes = 24 + 8 * (g.num_vertices + 1) + 4 * g.num_edges
     path = os.path.join(IO_DIR, "gb_io_bench.gshg")
@@ -73,6 +75,10 @@ def main():
                       "host_read_astype_s": t_host_read, "host_validate_s": t_host_validate,
                       "note": "page cache dropped before each read when permitted"}),
           flush=True)
+    text_bench()
+
+
+def text_bench():
     # edge-list text
     rng = np.random.default_rng(3)
     u = rng.integers(0, 1 << 26, size=N_LINES)
@@ -82,6 +88,17 @@ def main():
     gd = gb.load_edge_list(io.StringIO(text))
     torch.cuda.synchronize()
     t_dev = time.perf_counter() - t0
+    tpath = os.path.join(IO_DIR, "gb_io_bench.txt")
+    with open(tpath, "w") as f:
+        f.write(text)
+    os.system("sync; echo 3 > /proc/sys/vm/drop_caches 2>/dev/null")
+    t0 = time.perf_counter()
+    with open(tpath) as f:
+        gf = gb.load_edge_list(f)
+    torch.cuda.synchronize()
+    t_file = time.perf_counter() - t0
+    same = bool(np.array_equal(gf.orig_ids, gd.orig_ids)) and gf.num_edges == gd.num_edges
+    os.remove(tpath)
     sample = "\n".join(text.split("\n", N_LINES // 20)[: N_LINES // 20]) + "\n"
     t0 = time.perf_counter()
     gmod._parse_edge_lines_host(io.StringIO(sample))
@@ -90,6 +107,8 @@ def main():
                       "vertices": gd.num_vertices, "arcs": gd.num_edges,
                       "device_parse_densify_csr_s": t_dev,
                       "device_lines_per_s": N_LINES / t_dev,
+                      "file_byte_path_s": t_file, "file_lines_per_s": N_LINES / t_file,
+                      "file_equals_stringio": same,
                       "host_loop_s_extrapolated": t_host,
                       "host_loop_sample_lines": N_LINES // 20}), flush=True)
 
