@@ -6,6 +6,7 @@ device evaluator on a 1M+1M subsample).  Scores:
              (T=1 is bit-identical to the reference's default num_workers=1)
   gpu        the default device path (uncapped)
   gpu_cap<N> the device path with TrainConfig.max_inflight = N on every level
+  gpu_ppr[A] VERSE PPR positives (similarity="ppr", alpha 0.A, default 0.85)
 MODES (comma list) picks them, e.g. MODES=ref_w1,ref_w16,gpu,gpu_cap1024.
 """
 from __future__ import annotations
@@ -44,6 +45,11 @@ def main():
         t0 = time.perf_counter()
         if mode.startswith("ref_w"):
             M, _, _, _, _ = reference_embed(xh, ah, base, int(mode[5:]))
+        elif mode.startswith("gpu_ppr"):  # VERSE PPR positives, alpha = 0.<digits>
+            alpha = float("0." + mode[len("gpu_ppr"):]) if len(mode) > 7 else 0.85
+            cfg = dataclasses.replace(base, similarity="ppr", ppr_alpha=alpha)
+            M = setup.embed(cfg)
+            torch.cuda.synchronize()
         else:
             cfg = base if mode == "gpu" else dataclasses.replace(
                 base, max_inflight=int(mode[len("gpu_cap"):]))
