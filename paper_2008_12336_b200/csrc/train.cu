@@ -220,9 +220,12 @@ static int train_passes_impl(int64_t num_vertices, const int64_t *xadj, const in
       // GB_TRAIN_FAST_SIGMOID)
       if (on && var.pass_staged_hot && (use_hot(flags) || use_hot_f64(flags)) && !ppr)
         var.pass = var.pass_staged_hot;
+      else if (on && ppr && var.pass_staged_hot_ppr && use_hot_f64(flags))
+        var.pass = var.pass_staged_hot_ppr;  // PPR walk in the staged HOT pass
       fn = var.pass;
     }
-    const bool staged = var.pass && var.pass == var.pass_staged_hot;
+    const bool staged = var.pass && (var.pass == var.pass_staged_hot ||
+                                     var.pass == var.pass_staged_hot_ppr);
     if (staged) {
       smem = (size_t)(kBlock / var.G) * kChunk * dim * sizeof(float);
       GB_CUDA_TRY(cudaFuncSetAttribute((const void *)var.pass,

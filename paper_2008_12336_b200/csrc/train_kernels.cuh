@@ -479,18 +479,26 @@ __device__ __forceinline__ void run_chunk(Row &S, int64_t src_row, const int32_t
 // registers held while in flight) and come to registers one at a time when
 // they train; sample 0 (the positive, whose address arrives last through the
 // xadj -> adj chain) is loaded straight into registers.
-template <class Row>
+// Walk (PPR passes): ids[0] is resolved by the given walk after rows 1..3
+// are in flight, so the walk's dependent xadj/adj loads overlap their copies.
+struct NoWalk {
+  __device__ __forceinline__ int32_t operator()() const { return -1; }
+};
+
+template <class Row, class Walk = NoWalk>
 __device__ __forceinline__ void run_chunk_staged(Row &S, int64_t src_row,
-                                                 const int32_t (&ids)[kChunk], unsigned pos_mask,
+                                                 int32_t (&ids)[kChunk], unsigned pos_mask,
                                                  float *__restrict__ Mtgt, int dim, double lr,
                                                  float *slots, const GroupCtx &g, bool &bad,
                                                  bool fast, bool atomic, bool self_possible = true,
-                                                 bool load_once = false) {
+                                                 bool load_once = false, Walk walk = Walk(),
+                                                 bool do_walk = false) {
 #pragma unroll
   for (int j = 1; j < kChunk; ++j)
     if (ids[j] >= 0 && !(self_possible && ids[j] == src_row))
       Row::stage(slots + j * dim, Mtgt + (int64_t)ids[j] * dim, g.gl);
   asm volatile("cp.async.commit_group;" ::: "memory");
+  if (do_walk) ids[0] = walk();
   Row R;
   if (ids[0] >= 0 && !(self_possible && ids[0] == src_row))
     R.load(Mtgt + (int64_t)ids[0] * dim, g.gl, dim);
@@ -798,8 +806,10 @@ __device__ __forceinline__ void train_source(const PassArgs &a, const GroupCtx &
 // the runtime-flag branches otherwise triple the unrolled code, and the
 // i-cache misses that cost show up as the top ncu stall (no_instructions).
 // F64S (with HOT): the same compile-time flags but the reference's fp64
-// sigmoid and divide (trainer.py:118) instead of the fp32 one.
-template <class Row, bool EXACT, int KIND, bool HOT, bool F64S = false>
+// sigmoid and divide (trainer.py:118) instead of the fp32 one.  PPRW (KIND 3
+// only): positives from the PPR walk (ppr_positive) instead of a uniform
+// neighbour.
+template <class Row, bool EXACT, int KIND, bool HOT, bool F64S = false, bool PPRW = false>
 __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 ? 3 : Row::kMinBlocks))
     train_passes_kernel(PassArgs a) {
   constexpr int G = Row::G;
@@ -845,13 +855,21 @@ __global__ void __launch_bounds__(kBlock, (KIND == 1 || EXACT) ? 1 : (KIND == 3 
             const int idx = c0 + j;
             if (idx >= nsamp)
               ids[j] = -1;
-            else if (idx == 0)
-              ids[j] = __ldg(a.adj + x0 + draw_below(key, 0, deg));
+            else if (idx == 0)  // PPRW: resolved by the walk inside the chunk
+              ids[j] = PPRW ? 0 : __ldg(a.adj + x0 + draw_below(key, 0, deg));
             else
               ids[j] = (int32_t)draw_below(key, (uint64_t)idx, a.V);
           }
-          run_chunk_staged<Row>(S, v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, slots, g, bad_src,
-                                fast, atomic);
+          if constexpr (PPRW) {
+            const auto walk = [&]() {
+              return ppr_positive(a.xadj, a.adj, v, (double)a.ppr_alpha, key);
+            };
+            run_chunk_staged<Row>(S, v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, slots, g,
+                                  bad_src, fast, atomic, true, false, walk, c0 == 0);
+          } else {
+            run_chunk_staged<Row>(S, v, ids, c0 == 0 ? 1u : 0u, a.M, a.dim, lr, slots, g,
+                                  bad_src, fast, atomic);
+          }
         }
         keep.writeback(S, a.M + v * (int64_t)a.dim, g.gl, a.dim, atomic && !EXACT);
         if (bad_src) {
@@ -1316,6 +1334,7 @@ struct Variant {
   PassFn pass_ahead_hot = nullptr;  // KIND 2
   PassFn pass_staged_hot = nullptr;  // KIND 3
   PassFn pass_staged_hot_f64 = nullptr;  // KIND 3 with the fp64 sigmoid
+  PassFn pass_staged_hot_ppr = nullptr;  // KIND 3, fp64 sigmoid, PPR positives
   PassFn pass_hot_f64 = nullptr;
   PassFn pass_ahead_hot_f64 = nullptr;
   PassFn pass_pipe_hot_f64 = nullptr;
@@ -1344,6 +1363,7 @@ Variant make_variant() {
     v.pass_ahead_hot = train_passes_kernel<Row, false, 2, true>;
     v.pass_staged_hot = train_passes_kernel<Row, false, 3, true>;
     v.pass_staged_hot_f64 = train_passes_kernel<Row, false, 3, true, true>;
+    v.pass_staged_hot_ppr = train_passes_kernel<Row, false, 3, true, true, true>;
     v.pass_hot_f64 = train_passes_kernel<Row, false, 0, true, true>;
     v.pass_ahead_hot_f64 = train_passes_kernel<Row, false, 2, true, true>;
     v.pass_pipe_hot_f64 = train_passes_kernel<Row, false, 1, true, true>;

@@ -79,3 +79,20 @@ def test_hogwild_ppr_and_part_pair_rejection(cuda, orc):
     assert st.updates > 0 and bool(torch.isfinite(M).all())
     with pytest.raises(gb.ConfigError):
         gb.train_tournament(g, M, cfg, 1, num_ranks=2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d", [32, 128])
+def test_hot_ppr_pass_single_group_matches_sequential(cuda, orc, monkeypatch, d):
+    """The staged HOT pass with PPR positives (fp64 sigmoid), one source in
+    flight, is the oracle's sequential PPR pass up to the tree dot."""
+    monkeypatch.setenv("GB_PASS_SMEM", "1")
+    x, a = orc.rmat_graph(10, 6000, 4, densify_ids=True)
+    g = Graph(len(x) - 1, int(x[-1]), xadj=x, adj=a)
+    M0 = orc.init_embedding(g.num_vertices, d, 2) * 20.0
+    ref = M0.copy()
+    orc.train_level(x, a, ref, d, 2, 0.035, 3, 1, 0, ppr_alpha=0.85)
+    M = M0.copy()
+    gb.train_level(g, M, gb.TrainConfig(dim=d, similarity="ppr", max_inflight=1), 2)
+    err = np.abs(M - ref).max() / np.abs(ref).max()
+    assert err <= 1e-5, err
