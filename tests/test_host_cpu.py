@@ -334,3 +334,37 @@ def test_pair_side_pool_modes_and_balanced_config(monkeypatch):
         PairSides(csr, gb.TrainConfig(), 0, 5, st)
     with pytest.raises(gb.ConfigError):
         gb.TrainConfig(balanced_pools=True, deterministic=True).validate()
+
+
+def test_round2_entry_points_reject_bad_arguments_without_gpu():
+    """The round-2 entry points validate their arguments before touching the
+    device: null pointers / bad sizes give GB_E_INVALID and a message naming
+    the call (the reference's ValueError/ConfigError checks map to these)."""
+    import ctypes as C
+    L = _lib.load()
+    sz = C.c_size_t(0)
+    n = C.c_int64(0)
+    res = (C.c_int64 * 5)()
+    flags = C.c_int(0)
+    cases = [
+        ("gb_collapse_cas", lambda: L.gb_collapse_cas(0, None, None, None, 1.0, 1, None,
+                                                      C.byref(n), None, 0, None)),
+        ("gb_collapse_cas_workspace", lambda: L.gb_collapse_cas_workspace(0, C.byref(sz))),
+        ("gb_csr_validate", lambda: L.gb_csr_validate(-1, 0, None, None, C.byref(flags), None,
+                                                      0, None)),
+        ("gb_parse_edge_text", lambda: L.gb_parse_edge_text(None, 10, None, None, res, None, 0,
+                                                            None)),
+        ("gb_unique_ids", lambda: L.gb_unique_ids(None, 0, None, C.byref(n), 1, None, 0, None)),
+        ("gb_train_passes_ppr", lambda: L.gb_train_passes_ppr(10, None, None, None, 0, None, 32,
+                                                              3, 1, 0, 0, 1, 1, None, 0, 0,
+                                                              None, 0.0, None)),
+        ("gb_fill_pool_compact_dp", lambda: L.gb_fill_pool_compact_dp(None, None, 0, 1, 0, 1, 5,
+                                                                      None, 0, None, None, None,
+                                                                      None)),
+        ("gb_train_pool_list_dp", lambda: L.gb_train_pool_list_dp(None, None, 32, None, None,
+                                                                  None, 1, 5, 0, 1, 3, None, 2,
+                                                                  0, 0, None, None)),
+    ]
+    for name, call in cases:
+        assert call() == _lib.GB_E_INVALID, name
+        assert name.encode().split(b"_workspace")[0] in L.gb_last_error(), name
