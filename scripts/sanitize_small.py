@@ -24,5 +24,8 @@ tn.train_tournament(g, M, gb.TrainConfig(dim=128, balanced_pools=True), 40, num_
 order = gb.coarsen.degree_order(g)
 gb.coarsen.collapse_map_parallel(g, order, 64, run_dependent=True)
 gb.load_edge_list(io.StringIO("1 2\n2 3\n# c\n3 4\n"))
+rep = gb.run_link_prediction(g, gb.TrainConfig(dim=32, total_epochs=20), eval_seed=1,
+                             evaluator="device")
+assert 0.0 <= rep.aucroc <= 1.0
 torch.cuda.synchronize()
 print("sanitize_small ok")
