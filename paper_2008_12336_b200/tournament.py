@@ -116,6 +116,21 @@ def pair_index(K: int) -> dict[tuple[int, int], int]:
     return {pr: i for i, pr in enumerate(rotation_pairs(K))}
 
 
+def round_lr(lr0: float, rot: int, ri: int, rotations: int, K: int) -> float:
+    """Learning rate of round ri of rotation rot: lr_at (trainer.py:179-181)
+    over rotations * K rounds, i.e. decaying within a rotation as the
+    in-memory pass decays within a level's epochs.  (train_large decays per
+    rotation, bigtrain.py:432; with the one or two rotations that CLI-default
+    budgets give a level, that keeps lr near lr0 for the whole level and the
+    sharded AUCROC drifts well above the in-memory path's.)"""
+    return lr_at(lr0, rot * K + ri, rotations * K)
+
+
+def pair_rounds(K: int) -> dict[tuple[int, int], int]:
+    """Round index of each pair within a rotation."""
+    return {pr: ri for ri, rnd in enumerate(tournament_rounds(K)) for pr in rnd}
+
+
 def tournament_rotations(g: Graph, cfg: TrainConfig, e_i: int, K: int, B: int) -> int:
     """train_large's rotation count (bigtrain.py:389-395)."""
     eff = e_i
@@ -566,6 +581,8 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
     index = pair_index(K)
     P = len(index)
     moves = shift_moves(K)
+    rnd_of = pair_rounds(K)
+    pairs_by_index = [pr for pr, _ in sorted(index.items(), key=lambda kv: kv[1])]
     vs = os.environ.get("GB_VIRTUAL_STREAMS", "auto")
     if vs not in ("auto", "0", "1"):
         raise ConfigError(f"GB_VIRTUAL_STREAMS={vs!r}: expected auto, 0 or 1")
@@ -630,8 +647,8 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
             seeds = np.array([_lib.u64(_derived_seed(cfg.seed, rng_stream, rot * P + q))
                               for q in range(P)], dtype=np.uint64)
             h[:, 0] = seeds.view(np.int64)
-            h[:, 1] = np.full(P, lr_at(cfg.learning_rate, rot, rotations),
-                              dtype=np.float64).view(np.int64)
+            h[:, 1] = np.array([round_lr(cfg.learning_rate, rot, rnd_of[pr], rotations, K)
+                                for pr in pairs_by_index], dtype=np.float64).view(np.int64)
             ptab.copy_(hbuf[k], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record()
@@ -653,7 +670,8 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
                 seed = _derived_seed(cfg.seed, rng_stream, rot * P + index[(a, b)])
                 prm = ptab.data_ptr() + 16 * index[(a, b)] if ptab is not None else None
                 lst.append((k, PairStep(a, b, lo_a, hi_a, lo_b, hi_b, seed,
-                                        lr_at(cfg.learning_rate, rot, rotations), prm)))
+                                        round_lr(cfg.learning_rate, rot, ri, rotations, K),
+                                        prm)))
             out.append((r, lst))
         return out
 

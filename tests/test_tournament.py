@@ -86,8 +86,9 @@ def _sequential_replay(orc, g, x, a, M, cfg, e_i, G, B=5, stream=0):
     rot = tn.tournament_rotations(g, cfg, e_i, K, B)
     idx = tn.pair_index(K)
     P = len(idx)
+    rnd_of = tn.pair_rounds(K)
     for r, (pa, pb) in tn.sequential_order(K, rot):
-        lr = gb.lr_at(cfg.learning_rate, r, rot)
+        lr = tn.round_lr(cfg.learning_rate, r, rnd_of[(pa, pb)], rot, K)
         seed = gb.bigtrain._derived_seed(cfg.seed, stream, r * P + idx[(pa, pb)])
         la, ha, lb, hb = int(bnd[pa]), int(bnd[pa + 1]), int(bnd[pb]), int(bnd[pb + 1])
         A = M[la:ha]
