@@ -964,7 +964,7 @@ def _broadcast(M: torch.Tensor, group) -> None:
 
 
 def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
-                             shard_levels: int = 2, batch_size: int = 5, group=None,
+                             shard_levels: int = 1, batch_size: int = 5, group=None,
                              num_ranks: int | None = None, hierarchy=None,
                              return_device: bool = False, balanced_pools: bool = True,
                              return_parts: bool = False, host_parts: bool = False,
@@ -973,10 +973,14 @@ def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
     """train_multilevel (trainer.py:252-288) with the finest `shard_levels`
     levels trained by the tournament across ranks.
 
-    shard_levels=2 (default): on C3 (edge-scaled, 1000 epochs, 8 ranks) the
-    finest two levels are 74% of the one-GPU time, projecting 2.5x on 8
-    GPUs at AUCROC +0.007 over the in-memory ladder; 1 level: 1.4x, +0.003;
-    3 levels: 3.9x, +0.012 (profiles/r02_c3_shard_levels.jsonl).
+    shard_levels=1 (default): the finest level only.  With the rotation lr
+    decaying per round (round_lr) it stays closest to the in-memory ladder's
+    AUCROC across the measured schedules (8 ranks; C3 vertex-pass +0.005,
+    C3 edge-scaled -0.002, friendster shape vertex-pass -0.007; C1 over 30
+    paired seeds +0.002 / +0.005 at 2 / 4 ranks); 2 / 3 levels project 2.5x /
+    3.9x instead of 1.4x on 8 GPUs for C3 edge-scaled but drift further
+    (profiles/r02_c3_shard_levels_round_decay.jsonl,
+    r02_c1_sharded_aucroc_round_decay.jsonl, r02_c4_sharded_round_decay.jsonl).
 
     Every rank coarsens (the device collapse is deterministic, so the
     hierarchies are identical with no communication).  Levels above the

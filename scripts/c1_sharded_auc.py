@@ -15,6 +15,7 @@ import paper_2008_12336_b200 as gb  # noqa: E402
 from paper_2008_12336_b200.evaluate import LinkPredictionSetup, aucroc_parity_interval  # noqa: E402
 
 RANKS = [int(x) for x in os.environ.get("RANKS", "4").split(",")]
+SHARD = int(os.environ.get("SHARD", "2"))
 N = int(os.environ.get("NSEEDS", "30"))
 with open(os.path.join(ROOT, "tests", "golden", "c1_reference_auc.json")) as f:
     ref = json.load(f)
@@ -35,10 +36,11 @@ for R in [0] + RANKS:
             M = setup.embed(cfg)
         else:
             M, _ = gb.train_multilevel_sharded(setup.train_graph, cfg, hierarchy=setup.hierarchy,
-                                               num_ranks=R, return_device=True)
+                                               num_ranks=R, return_device=True,
+                                               shard_levels=SHARD)
         mine.append(setup.score(M))
     d = np.array(mine) - np.array([runs[s] for s in seeds])
-    print(json.dumps({"ranks": R, "mode": "in-memory" if R == 0 else "sharded (2 levels)",
+    print(json.dumps({"ranks": R, "mode": "in-memory" if R == 0 else f"sharded ({SHARD} levels)",
                       "n": len(seeds), "mean": float(np.mean(mine)),
                       "ref_mean": float(np.mean([runs[s] for s in seeds])),
                       "paired": aucroc_parity_interval(d)}), flush=True)

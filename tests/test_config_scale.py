@@ -151,11 +151,12 @@ def test_c1_aucroc_parity_with_reference(cuda):
 
 
 def test_c1_sharded_aucroc_parity_with_reference(cuda):
-    """The multi-GPU path (train_multilevel_sharded: balanced pools, two
-    sharded levels, here 2 virtual ranks = K=4 parts) on the same C1
-    protocol, paired with the reference's seeds: the north star's AUCROC bar
-    holds for the sharded path too (30 seeds at 2/4/8 ranks: +0.0019 /
-    +0.0048 / +0.0044, profiles/r02_c1_sharded_aucroc_parity.jsonl)."""
+    """The multi-GPU path (train_multilevel_sharded defaults: balanced pools,
+    the finest level sharded, lr decaying per round; here 2 virtual ranks =
+    K=4 parts) on the same C1 protocol, paired with the reference's seeds:
+    the north star's AUCROC bar holds for the sharded path too (30 seeds at
+    2 / 4 ranks: +0.0022 / +0.0047, CI inside +-0.01;
+    profiles/r02_c1_sharded_aucroc_round_decay.jsonl)."""
     ref, pr, setup = _c1_setup()
     runs = {r["seed"]: r["aucroc"] for r in ref["runs"]}
     seeds = sorted(runs)[:24]

@@ -429,7 +429,7 @@ def _gloo_gpu_worker(rank, world, port, out_path, what):
         else:
             cfg = gb.TrainConfig(dim=32, total_epochs=30, negative_samples=3, seed=4,
                                  deterministic=True)
-            M, _ = gb.train_multilevel_sharded(g, cfg)
+            M, _ = gb.train_multilevel_sharded(g, cfg, shard_levels=2)
             np.save(f"{out_path}.{rank}.npy", M)
     finally:
         dist.destroy_process_group()
@@ -477,6 +477,6 @@ def test_gloo_processes_on_one_gpu_sharded_multilevel(cuda, orc):
         g, x, a = _graph(orc, scale=10, samples=6000)
         cfg = gb.TrainConfig(dim=32, total_epochs=30, negative_samples=3, seed=4,
                              deterministic=True)
-        ref, _ = gb.train_multilevel_sharded(g, cfg, num_ranks=2)
+        ref, _ = gb.train_multilevel_sharded(g, cfg, num_ranks=2, shard_levels=2)
         for r in range(2):
             assert np.array_equal(np.load(f"{out}.{r}.npy"), ref), r
