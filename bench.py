@@ -200,7 +200,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": el * 1000.0 / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows / f64 dot",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows / f64 dot / f64 sigmoid",
         "data": "synthetic R-MAT (CPU generator, bit-identical to the GPU one)",
         "config": workload_config(),
         "details": {"parallelism": f"{threads} host threads"},
@@ -603,7 +603,7 @@ def run_sharded(args):
         "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32 rows / f64 dot / f32 sigmoid",
+        "dtype": "f32 rows / f64 dot / f64 sigmoid",
         "data": "synthetic R-MAT generated on device (seeded, Graph500 parameters)",
         "config": sharded_config(),
         "details": {"K": K, "vertices": g.num_vertices, "arcs": g.num_edges,
@@ -661,7 +661,7 @@ def run_sharded_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1000.0 / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32 rows / f64 dot", "data": "synthetic R-MAT (CPU generator, bit-identical "
+        "dtype": "f32 rows / f64 dot / f64 sigmoid", "data": "synthetic R-MAT (CPU generator, bit-identical "
                                               "to the GPU one)",
         "config": sharded_config(),
         "details": {"parallelism": f"{threads} host threads", "K": K},
@@ -730,7 +730,7 @@ def run_tournament(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32 rows / f64 dot",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32 rows / f64 dot / f64 sigmoid",
         "data": "synthetic R-MAT generated on device (seeded, Graph500 parameters)",
         "config": ({
             "workload": f"part-pair tournament on the C2 graph, K={K} parts, B={B}, d={dim}",
