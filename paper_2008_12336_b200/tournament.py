@@ -530,8 +530,8 @@ def _graph_key(g: Graph, store: "PartStore", cfg: TrainConfig, B: int, streams: 
     bufs = tuple((p, store.data[p].data_ptr()) for r in store.local for p in store.parts[r])
     return (str(store.device), g.num_vertices, g.num_edges, x.data_ptr(), a.data_ptr(),
             store.V, store.d, store.G, tuple(store.local), bufs, streams, B,
-            cfg.dim, cfg.negative_samples, cfg.reuse_updated_source, cfg.deterministic,
-            cfg.atomic_rows, cfg.balanced_pools, cfg.max_inflight,
+            cfg.dim, cfg.negative_samples, _train_flags(cfg, pair=True), cfg.balanced_pools,
+            cfg.max_inflight,
             os.environ.get("GB_POOL_MODE", "compact"))
 
 

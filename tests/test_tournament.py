@@ -222,6 +222,26 @@ def test_rotation_graph_deterministic_bit_exact(cuda, orc, G, monkeypatch):
 
 
 @pytest.mark.gpu
+def test_rotation_graph_cache_keyed_on_kernel_flags(cuda, orc, monkeypatch):
+    """The captured launches bake in the kernel flags, so a call whose flags
+    differ (here the sigmoid flavour) must capture afresh instead of
+    replaying the cached graph."""
+    g, x, a = _graph(orc, scale=10, samples=6000)
+    monkeypatch.setenv("GB_ROTATION_GRAPH", "1")
+    tn.clear_rotation_graphs()
+    M0 = orc.init_embedding(g.num_vertices, 32, 2)
+    keys = []
+    for fast in (True, False):
+        cfg = gb.TrainConfig(dim=32, negative_samples=3, seed=4, fast_sigmoid=fast)
+        M = torch.from_numpy(M0.copy()).cuda()
+        tn.train_tournament(g, M, cfg, 60, num_ranks=2)
+        assert len(tn._ROTATION_GRAPHS) == 1
+        keys.append(next(iter(tn._ROTATION_GRAPHS)))
+    assert keys[0] != keys[1]
+    tn.clear_rotation_graphs()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("balanced", [False, True])
 def test_rotation_graph_hogwild_matches_eager(cuda, orc, monkeypatch, balanced):
     """Default (Hogwild) pools: the graph-replayed rotations draw exactly the
