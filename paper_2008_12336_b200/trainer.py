@@ -82,9 +82,10 @@ class TrainConfig:
     ppr_alpha: float = 0.85
     # parallel kernels' sigmoid: False = fp64 like the reference
     # (trainer.py:118), True = fp32 cancellation-free form (~1e-7 relative),
-    # None = auto: fp64 in the vertex passes (no cost: 5.44 vs 5.44 G upd/s
-    # on C2), fp32 in the part-pair kernels (6% faster at K=2;
-    # profiles/r02_sigmoid_fp64_vs_fp32.jsonl)
+    # None (default) / False: the reference's fp64 sigmoid in vertex passes
+    # and part-pair kernels (no cost on C2 or the K=16 tournament, 6% at the
+    # power-capped K=2; profiles/r02_sigmoid_fp64_vs_fp32.jsonl,
+    # r02_pair_sigmoid_default_fp64.jsonl); True: the fp32 form
     fast_sigmoid: bool | None = FAST_SIGMOID_DEFAULT
 
     def validate(self) -> None:
