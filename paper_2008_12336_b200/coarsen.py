@@ -198,9 +198,15 @@ def build_coarse_graph(g: Graph, m: Mapping, num_workers: int = 1,
         _lib.call("gb_mapped_histogram", _lib.ptr(xadj), _lib.ptr(adj), V, _lib.ptr(cmap),
                   _lib.ptr(hist), st)
 
+        starts = torch.cumsum(hist, 0) - hist  # each row's first key (exclusive scan)
+
         def fill(c0, c1, keys, cursor):
-            _lib.call("gb_mapped_keys_range", _lib.ptr(xadj), _lib.ptr(adj), V, _lib.ptr(cmap),
-                      nc, c0, c1, _lib.ptr(keys), _lib.ptr(cursor), st)
+            # per-row cursors (gb_mapped_keys_rows): the block's rows start at
+            # their scanned offsets, so the appends spread over the rows
+            row_cursor = starts[c0:c1] - starts[c0]
+            _lib.call("gb_mapped_keys_rows", _lib.ptr(xadj), _lib.ptr(adj), V, _lib.ptr(cmap),
+                      nc, c0, c1, _lib.ptr(row_cursor), _lib.ptr(keys), st)
+            cursor.copy_(hist[c0:c1].sum().reshape(1))
 
         return csr_from_blocks(nc, nc, hist, fill, max_block_keys, directed=g.directed)
     ws, wsb = _lib.workspace("gb_coarse_csr_workspace", V, E, nc)

@@ -979,6 +979,49 @@ __global__ void mapped_keys_range_kernel(const int64_t *__restrict__ xadj,
   }
 }
 
+// Same keys as mapped_keys_range_kernel, appended per ROW: row_cursor[r]
+// (r = cluster - c0) starts at the row's offset in the block's key buffer (an
+// exclusive scan of gb_mapped_histogram over the block) and ends at the next
+// row's.  The single block-wide cursor serialised every 32-key append on one
+// L2 address (~60 ms per 1G keys at the C5 shape); per-row cursors spread
+// them over the block's rows.  Each warp tests the clusters of 32 of its
+// vertices at once (warp w owns vertices w, w + nwarps, ...: the hubs, which
+// lead the rank-ordered ids of a coarse level, stay spread over the warps).
+__global__ void mapped_keys_rows_kernel(const int64_t *__restrict__ xadj,
+                                        const int32_t *__restrict__ adj,
+                                        const int32_t *__restrict__ cmap, int64_t V, int64_t c0,
+                                        int64_t c1, uint64_t nc, uint64_t *__restrict__ keys,
+                                        unsigned long long *__restrict__ row_cursor) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned lt = lanemask_lt();
+  for (int64_t vb = warp; vb < V; vb += nwarps * 32) {
+    const int64_t vl = vb + (int64_t)lane * nwarps;
+    const int32_t cl = vl < V ? cmap[vl] : -1;
+    unsigned in_range = __ballot_sync(0xffffffffu, vl < V && cl >= c0 && cl < c1);
+    while (in_range) {
+      const int src_lane = __ffs(in_range) - 1;
+      in_range &= in_range - 1;
+      const int64_t v = vb + (int64_t)src_lane * nwarps;
+      const int64_t cv = __shfl_sync(0xffffffffu, cl, src_lane);
+      const int64_t e0 = xadj[v], e1 = xadj[v + 1];
+      for (int64_t eb = e0; eb < e1; eb += 32) {
+        const int64_t e = eb + lane;
+        int64_t cu = cv;
+        if (e < e1) cu = cmap[adj[e]];
+        const bool emit = cu != cv;
+        const unsigned m = __ballot_sync(0xffffffffu, emit);
+        if (!m) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(row_cursor + (cv - c0), (unsigned long long)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (emit) keys[base + __popc(m & lt)] = (uint64_t)(cv - c0) * nc + (uint64_t)cu;
+      }
+    }
+  }
+}
+
 // rows [r0, r1) of xadj from the block's sorted unique keys (row-relative)
 __global__ void xadj_rows_from_keys(const uint64_t *__restrict__ keys, int64_t nkeys,
                                     int64_t rows, uint64_t ncols, int64_t base,
@@ -1044,6 +1087,23 @@ GB_API int gb_mapped_keys_range(const int64_t *xadj, const int32_t *adj, int64_t
   mapped_keys_range_kernel<<<std::max(blocks, 1), 256, 0, as_stream(stream_handle)>>>(
       xadj, adj, cmap, num_vertices, c0, c1, (uint64_t)num_clusters, keys,
       reinterpret_cast<unsigned long long *>(cursor));
+  GB_CHECK_LAUNCH();
+  return GB_OK;
+}
+
+GB_API int gb_mapped_keys_rows(const int64_t *xadj, const int32_t *adj, int64_t num_vertices,
+                               const int32_t *cmap, int64_t num_clusters, int64_t c0,
+                               int64_t c1, int64_t *row_cursor, uint64_t *keys,
+                               void *stream_handle) {
+  GB_REQUIRE(num_vertices >= 1 && xadj && cmap && keys && row_cursor && c0 >= 0 && c1 >= c0 &&
+                 c1 <= num_clusters,
+             "gb_mapped_keys_rows: bad args");
+  if (c1 == c0) return GB_OK;
+  const int blocks =
+      (int)std::min<int64_t>((num_vertices + 255) / 256, (int64_t)num_sms() * 16);
+  mapped_keys_rows_kernel<<<std::max(blocks, 1), 256, 0, as_stream(stream_handle)>>>(
+      xadj, adj, cmap, num_vertices, c0, c1, (uint64_t)num_clusters, keys,
+      reinterpret_cast<unsigned long long *>(row_cursor));
   GB_CHECK_LAUNCH();
   return GB_OK;
 }

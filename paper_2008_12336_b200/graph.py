@@ -16,7 +16,10 @@ edges as the reference for the same seed.
 from __future__ import annotations
 
 import ctypes as C
+import json
+import os
 import struct
+import time
 from dataclasses import dataclass
 from typing import IO, Iterable
 
@@ -227,29 +230,58 @@ def csr_from_blocks(num_rows: int, num_cols: int, hist: torch.Tensor, fill_block
     cursor)` appends the keys of the block's arcs (gb_arc_keys_range /
     gb_mapped_keys_range over every batch).  Equal to the one-shot build bit
     for bit: blocks emit their rows in order."""
+    trace = os.environ.get("GB_TRACE_BLOCKS")
+    ts = [time.perf_counter()]
     h = hist.cpu().numpy()
+    ts.append(time.perf_counter())
     upper = int(h.sum())
     blocks = plan_row_blocks(h, max_block_keys)
     block_keys = int(max((h[a:b].sum() for a, b in blocks), default=0))
+    ts.append(time.perf_counter())
     xadj = torch.empty(num_rows + 1, dtype=torch.int64, device="cuda")
     adj = torch.empty(max(upper, 1), dtype=torch.int32, device="cuda")
     keys = torch.empty(max(block_keys, 1), dtype=torch.int64, device="cuda")
     cursor = torch.zeros(1, dtype=torch.int64, device="cuda")
     rows_max = max((b - a for a, b in blocks), default=1)
+    if trace:
+        torch.cuda.synchronize()
+    ts.append(time.perf_counter())
     ws, wsb = _lib.workspace("gb_keys_to_rows_workspace", max(block_keys, 1), rows_max, num_cols)
     base = 0
+    if trace:
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter())
+        print(json.dumps({"blocks": len(blocks), "rows": num_rows, "upper_keys": upper,
+                          "hist_download_ms": 1e3 * (ts[1] - ts[0]),
+                          "plan_ms": 1e3 * (ts[2] - ts[1]),
+                          "alloc_out_keys_ms": 1e3 * (ts[3] - ts[2]),
+                          "alloc_workspace_ms": 1e3 * (ts[4] - ts[3]),
+                          "alloc_gib": round((8 * num_rows + 4 * upper + 8 * block_keys + wsb)
+                                             / 2**30, 1),
+                          "reserved_gib": round(torch.cuda.memory_reserved() / 2**30, 1)}),
+              flush=True)
     for r0, r1 in blocks:
+        t0 = time.perf_counter() if trace else 0.0
         cursor.zero_()
         fill_block(r0, r1, keys, cursor)
         nk = int(cursor.item())
+        t1 = time.perf_counter() if trace else 0.0
         nu = C.c_int64(0)
         _lib.call("gb_keys_to_rows", _lib.ptr(keys), nk, r1 - r0, num_cols, base,
                   xadj.data_ptr() + r0 * 8, adj.data_ptr() + base * 4, C.byref(nu),
                   _lib.ptr(ws), wsb, _lib.stream())
         base += int(nu.value)
+        if trace:  # per-block phases (scripts/profile_coarsen.py)
+            print(json.dumps({"block": [r0, r1], "keys": nk, "unique": int(nu.value),
+                              "fill_ms": 1e3 * (t1 - t0),
+                              "sort_ms": 1e3 * (time.perf_counter() - t1)}), flush=True)
+    t_end = time.perf_counter()
     xadj[num_rows] = base
     del ws, keys
     adj = adj[: max(base, 1)].clone() if upper > 1.25 * max(base, 1) else adj
+    if trace:
+        torch.cuda.synchronize()
+        print(json.dumps({"finish_ms": 1e3 * (time.perf_counter() - t_end)}), flush=True)
     return Graph(num_rows, base, directed=directed, orig_ids=orig_ids, xadj_dev=xadj,
                  adj_dev=adj)
 

@@ -208,10 +208,14 @@ def test_blocked_arc_batches_equal_from_edges(cuda):
     assert np.array_equal(got.xadj, ref.xadj) and np.array_equal(got.adj, ref.adj)
 
 
-def test_blocked_coarsening_equals_one_shot(cuda, orc):
+@pytest.mark.parametrize("cap", [100_000, 3_000])
+def test_blocked_coarsening_equals_one_shot(cuda, orc, cap):
+    """Row blocks (per-row key cursors, gb_mapped_keys_rows) build the same
+    hierarchy as the one-shot coarse CSR; cap 3,000 puts hub rows above the
+    cap in blocks of their own."""
     g = gb.rmat_graph(16, 1 << 20, 5, densify_ids=True)
     h1 = gb.coarsen_all(g, threshold=100)
-    h2 = gb.coarsen_all(g, threshold=100, max_block_keys=100_000)
+    h2 = gb.coarsen_all(g, threshold=100, max_block_keys=cap)
     assert h1.depth == h2.depth
     for L in range(h1.depth):
         assert np.array_equal(h1.graphs[L].xadj, h2.graphs[L].xadj), L
