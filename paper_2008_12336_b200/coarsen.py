@@ -182,12 +182,13 @@ def collapse_map_parallel(g: Graph, order, num_workers: int,
 
 
 def build_coarse_graph(g: Graph, m: Mapping, num_workers: int = 1,
-                       max_block_keys: int | None = None) -> Graph:
+                       max_block_keys: int | None = None, scratch: dict | None = None) -> Graph:
     """Contract g along m: clusters become vertices, parallel arcs merged,
     self-loops dropped, rows sorted (coarsen.py:256-281).  max_block_keys
     builds the coarse rows block by block (gb_mapped_keys_range +
     gb_keys_to_rows) so the key scratch is bounded instead of 24 B per arc;
-    the result is identical."""
+    the result is identical.  `scratch` (a dict) keeps the block key buffer and
+    workspace for the next level's build."""
     xadj, adj = g.device_csr()
     cmap = m.device_map()
     V, E, nc = g.num_vertices, g.num_edges, m.num_clusters
@@ -208,7 +209,8 @@ def build_coarse_graph(g: Graph, m: Mapping, num_workers: int = 1,
                       nc, c0, c1, _lib.ptr(row_cursor), _lib.ptr(keys), st)
             cursor.copy_(hist[c0:c1].sum().reshape(1))
 
-        return csr_from_blocks(nc, nc, hist, fill, max_block_keys, directed=g.directed)
+        return csr_from_blocks(nc, nc, hist, fill, max_block_keys, directed=g.directed,
+                               scratch=scratch)
     ws, wsb = _lib.workspace("gb_coarse_csr_workspace", V, E, nc)
     x2 = torch.empty(nc + 1, dtype=torch.int64, device="cuda")
     a2 = torch.empty(max(E, 1), dtype=torch.int32, device="cuda")
@@ -235,6 +237,7 @@ def coarsen_all(g: Graph, threshold: int = 100, num_workers: int = 1,
     if num_workers < 1:
         raise ConfigError("num_workers must be >= 1")
     graphs, mappings, level_ms, rounds = [g], [], [], []
+    scratch: dict = {}  # row-block key buffer + workspace, shared by the levels
     stalled = False
     while graphs[-1].num_vertices > threshold:
         cur = graphs[-1]
@@ -247,7 +250,7 @@ def coarsen_all(g: Graph, threshold: int = 100, num_workers: int = 1,
         if m.num_clusters > STALL_RATIO * cur.num_vertices:
             stalled = True
             break
-        nxt = build_coarse_graph(cur, m, max_block_keys=max_block_keys)
+        nxt = build_coarse_graph(cur, m, max_block_keys=max_block_keys, scratch=scratch)
         torch.cuda.current_stream().synchronize()
         level_ms.append((time.perf_counter() - t0) * 1000.0)
         graphs.append(nxt)

@@ -222,8 +222,48 @@ def plan_row_blocks(hist: np.ndarray, max_block_keys: int) -> list[tuple[int, in
     return blocks
 
 
+def plan_row_blocks_tensor(hist: torch.Tensor, max_block_keys: int):
+    """plan_row_blocks on a torch tensor where it lives (the device histogram
+    of a C5-sized CSR has 2^28 rows: a 2 GB download plus host cumsum costs
+    seconds): (blocks, total keys, largest block's keys).  Same blocks as
+    plan_row_blocks."""
+    if max_block_keys < 1:
+        raise ValueError("max_block_keys must be positive")
+    n = int(hist.shape[0])
+    if n == 0:
+        return [], 0, 0
+    csum = torch.cumsum(hist.to(torch.int64), 0)  # csum[i] = keys of rows [0, i]
+    upper = int(csum[-1])
+    blocks, r0, before, largest = [], 0, 0, 0
+    while r0 < n:
+        target = torch.tensor([before + max_block_keys], dtype=torch.int64, device=csum.device)
+        r1 = int(torch.searchsorted(csum, target, right=True))
+        r1 = min(max(r1, r0 + 1), n)
+        after = int(csum[r1 - 1])
+        blocks.append((r0, r1))
+        largest = max(largest, after - before)
+        r0, before = r1, after
+    return blocks, upper, largest
+
+
+def _scratch_buffer(scratch: dict | None, name: str, numel: int, dtype) -> torch.Tensor:
+    """A device buffer of at least numel elements, kept in `scratch` between
+    row-block builds (a coarsening ladder asks for the same tens of GiB at
+    every level; re-allocating them cost 0.2-1.1 s per level at C5)."""
+    if scratch is None:
+        return torch.empty(numel, dtype=dtype, device="cuda")
+    buf = scratch.get(name)
+    if buf is None or buf.numel() < numel:
+        scratch.pop(name, None)
+        del buf
+        buf = torch.empty(numel, dtype=dtype, device="cuda")
+        scratch[name] = buf
+    return buf[:numel]
+
+
 def csr_from_blocks(num_rows: int, num_cols: int, hist: torch.Tensor, fill_block,
-                    max_block_keys: int, directed: bool = False, orig_ids=None) -> Graph:
+                    max_block_keys: int, directed: bool = False, orig_ids=None,
+                    scratch: dict | None = None) -> Graph:
     """Row-block CSR construction (gb_keys_to_rows): rows are keyed, sorted,
     deduplicated and emitted one block at a time, so scratch scales with
     max_block_keys instead of the arc count.  `fill_block(r0, r1, keys,
@@ -232,27 +272,30 @@ def csr_from_blocks(num_rows: int, num_cols: int, hist: torch.Tensor, fill_block
     for bit: blocks emit their rows in order."""
     trace = os.environ.get("GB_TRACE_BLOCKS")
     ts = [time.perf_counter()]
-    h = hist.cpu().numpy()
+    if trace:
+        torch.cuda.synchronize()  # the histogram pass
     ts.append(time.perf_counter())
-    upper = int(h.sum())
-    blocks = plan_row_blocks(h, max_block_keys)
-    block_keys = int(max((h[a:b].sum() for a, b in blocks), default=0))
+    blocks, upper, block_keys = plan_row_blocks_tensor(hist, max_block_keys)
     ts.append(time.perf_counter())
     xadj = torch.empty(num_rows + 1, dtype=torch.int64, device="cuda")
     adj = torch.empty(max(upper, 1), dtype=torch.int32, device="cuda")
-    keys = torch.empty(max(block_keys, 1), dtype=torch.int64, device="cuda")
+    keys = _scratch_buffer(scratch, "keys", max(block_keys, 1), torch.int64)
     cursor = torch.zeros(1, dtype=torch.int64, device="cuda")
     rows_max = max((b - a for a, b in blocks), default=1)
     if trace:
         torch.cuda.synchronize()
     ts.append(time.perf_counter())
-    ws, wsb = _lib.workspace("gb_keys_to_rows_workspace", max(block_keys, 1), rows_max, num_cols)
+    n_ws = C.c_size_t(0)
+    _lib.call("gb_keys_to_rows_workspace", max(block_keys, 1), rows_max, num_cols,
+              C.byref(n_ws))
+    wsb = int(n_ws.value)
+    ws = _scratch_buffer(scratch, "ws", max(wsb, 1), torch.uint8)
     base = 0
     if trace:
         torch.cuda.synchronize()
         ts.append(time.perf_counter())
         print(json.dumps({"blocks": len(blocks), "rows": num_rows, "upper_keys": upper,
-                          "hist_download_ms": 1e3 * (ts[1] - ts[0]),
+                          "hist_ms": 1e3 * (ts[1] - ts[0]),
                           "plan_ms": 1e3 * (ts[2] - ts[1]),
                           "alloc_out_keys_ms": 1e3 * (ts[3] - ts[2]),
                           "alloc_workspace_ms": 1e3 * (ts[4] - ts[3]),

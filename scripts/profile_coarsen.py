@@ -48,6 +48,7 @@ print(json.dumps({"phase": "build", "V": g.num_vertices, "E": g.num_edges,
 t_all = time.perf_counter()
 cur = g
 lvl = 0
+scratch: dict = {}  # as coarsen_all: block buffers shared by the levels
 while cur.num_vertices > 100:
     t = [time.perf_counter()]
     order = cz._degree_order_dev(cur)
@@ -57,7 +58,7 @@ while cur.num_vertices > 100:
     if m.num_clusters > cz.STALL_RATIO * cur.num_vertices:
         break
     t_hist = time.perf_counter()
-    nxt = cz.build_coarse_graph(cur, m, max_block_keys=block)
+    nxt = cz.build_coarse_graph(cur, m, max_block_keys=block, scratch=scratch)
     torch.cuda.synchronize(); t.append(time.perf_counter())
     print(json.dumps({"level": lvl, "V": cur.num_vertices, "E": cur.num_edges,
                       "clusters": m.num_clusters, "coarse_E": nxt.num_edges, "rounds": r,

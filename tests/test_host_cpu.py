@@ -368,3 +368,27 @@ def test_round2_entry_points_reject_bad_arguments_without_gpu():
     for name, call in cases:
         assert call() == _lib.GB_E_INVALID, name
         assert name.encode().split(b"_workspace")[0] in L.gb_last_error(), name
+
+
+def test_row_block_plans_agree():
+    """The row-block planner (graph.py) on numpy and on a tensor: the same
+    consecutive blocks covering every row, each within the key cap unless it
+    is a single row above it."""
+    import torch
+
+    from paper_2008_12336_b200.graph import plan_row_blocks, plan_row_blocks_tensor
+    rng = np.random.default_rng(5)
+    for n, cap in ((1, 10), (1000, 50), (5000, 700), (777, 10_000)):
+        h = rng.integers(0, 40, size=n).astype(np.int64)
+        h[rng.integers(0, n, size=max(1, n // 100))] = 3 * cap  # rows above the cap
+        h[: min(n, 7)] = 0
+        ref = plan_row_blocks(h, cap)
+        got, upper, largest = plan_row_blocks_tensor(torch.from_numpy(h), cap)
+        assert got == ref, (n, cap)
+        assert upper == int(h.sum())
+        assert largest == max(int(h[a:b].sum()) for a, b in ref)
+        assert ref[0][0] == 0 and ref[-1][1] == n
+        for (a, b), (c, _) in zip(ref, ref[1:]):
+            assert b == c
+        for a, b in ref:
+            assert h[a:b].sum() <= cap or b - a == 1
