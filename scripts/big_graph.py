@@ -47,6 +47,8 @@ def out(**kw):
 
 
 torch.cuda.set_device(0)
+if os.environ.get("RESERVE", "0") == "1":  # map HBM once (memory.py; opt-in)
+    out(phase="reserve", **gb.reserve_device_memory(fraction=0.92))
 t0 = time.perf_counter()
 g = gb.rmat_graph(scale, samples, 7, densify_ids=True)
 torch.cuda.synchronize()

@@ -31,6 +31,9 @@ def gib():
 
 
 def main():
+    if os.environ.get("RESERVE", "0") == "1":  # map HBM once (memory.py; opt-in)
+        print(json.dumps({"phase": "reserve", **gb.reserve_device_memory(fraction=0.92)}),
+              flush=True)
     t0 = time.perf_counter()
     g = gb.rmat_graph(SCALE, SAMPLES, 7, densify_ids=True, max_block_keys=BLOCK)
     torch.cuda.synchronize()

@@ -39,6 +39,13 @@ def mempool_release_threshold(set_max=False):
 
 print(json.dumps({"release_threshold": mempool_release_threshold(bool(os.environ.get("RELEASE")))}),
       flush=True)
+if os.environ.get("WARM_GIB"):  # map the pool once up front (kept with RELEASE=1)
+    t_w = time.perf_counter()
+    warm = torch.empty(int(float(os.environ["WARM_GIB"]) * 2**30), dtype=torch.uint8, device="cuda")
+    del warm
+    torch.cuda.synchronize()
+    print(json.dumps({"warm_gib": float(os.environ["WARM_GIB"]),
+                      "warm_s": time.perf_counter() - t_w}), flush=True)
 t0 = time.perf_counter()
 g = gb.rmat_graph(scale, samples, 7, densify_ids=True, max_block_keys=block)
 g.device_csr()  # the CSR is built on first use
