@@ -42,9 +42,18 @@ def rmat_edges(scale: int, num_samples: int, seed: int, permute: bool = True,
     return src, dst
 
 
+def _samples_fit(scale: int, num_samples: int, max_block_keys: int) -> bool:
+    """Whether the int64 sample arrays fit beside the row-block build: the
+    samples (16 B each), the block's keys and workspace (~24 B per key), the
+    CSR (<= 8 B per sample in adj, 8 B per id in xadj) and 4 GiB of slack."""
+    free, _ = torch.cuda.mem_get_info()
+    need = 16 * num_samples + 24 * max_block_keys + 8 * num_samples + 8 * (1 << scale) + (4 << 30)
+    return need < free
+
+
 def rmat_graph(scale: int, num_samples: int, seed: int = 7, densify_ids: bool = False,
                permute: bool = True, max_block_keys: int | None = None,
-               batch_samples: int = 1 << 28) -> Graph:
+               batch_samples: int = 1 << 28, keep_samples: bool | None = None) -> Graph:
     """Undirected R-MAT CSR on the device.  With densify_ids, isolated ids
     are dropped (orig_ids holds the surviving raw ids).
 
@@ -52,7 +61,10 @@ def rmat_graph(scale: int, num_samples: int, seed: int = 7, densify_ids: bool = 
     with samples regenerated in batches of batch_samples for every block
     (each sample is a pure function of its index), so neither the sample
     arrays nor the key scratch scale with the graph -- the path for graphs
-    whose one-shot build exceeds one GPU (C5).  Same graph bit for bit."""
+    whose one-shot build exceeds one GPU (C5).  keep_samples (default: when
+    they fit, _samples_fit) generates the samples once and keeps them for
+    every block instead (C5: 69 GB; the nine block passes then read them
+    instead of regenerating 4.3B samples each).  Same graph bit for bit."""
     flags = _lib.GB_CSR_DROP_SELF | _lib.GB_CSR_SYMMETRIZE
     if max_block_keys is not None:
         from .graph import csr_from_arc_batches
@@ -66,16 +78,32 @@ def rmat_graph(scale: int, num_samples: int, seed: int = 7, densify_ids: bool = 
                       _lib.ptr(ws), wsb, _lib.stream())
             del ws
         bs = max(1, min(batch_samples, num_samples))
-        src = torch.empty(bs, dtype=torch.int64, device="cuda")
-        dst = torch.empty(bs, dtype=torch.int64, device="cuda")
-
-        def batches():
+        if keep_samples is None:
+            keep_samples = _samples_fit(scale, num_samples, max_block_keys)
+        if keep_samples:  # generate once, every block reads them
+            src = torch.empty(num_samples, dtype=torch.int64, device="cuda")
+            dst = torch.empty(num_samples, dtype=torch.int64, device="cuda")
             for first in range(0, num_samples, bs):
                 n = min(bs, num_samples - first)
                 _lib.call("gb_rmat_edges_range", scale, first, n, a, a + b, a + b + c,
-                          _lib.u64(seed), _lib.ptr(perm), _lib.ptr(src), _lib.ptr(dst),
-                          _lib.stream())
-                yield src[:n], dst[:n]
+                          _lib.u64(seed), _lib.ptr(perm), src.data_ptr() + 8 * first,
+                          dst.data_ptr() + 8 * first, _lib.stream())
+
+            def batches():
+                for first in range(0, num_samples, bs):
+                    n = min(bs, num_samples - first)
+                    yield src[first:first + n], dst[first:first + n]
+        else:
+            src = torch.empty(bs, dtype=torch.int64, device="cuda")
+            dst = torch.empty(bs, dtype=torch.int64, device="cuda")
+
+            def batches():
+                for first in range(0, num_samples, bs):
+                    n = min(bs, num_samples - first)
+                    _lib.call("gb_rmat_edges_range", scale, first, n, a, a + b, a + b + c,
+                              _lib.u64(seed), _lib.ptr(perm), _lib.ptr(src), _lib.ptr(dst),
+                              _lib.stream())
+                    yield src[:n], dst[:n]
 
         g = csr_from_arc_batches(1 << scale, batches, flags, max_block_keys)
         del src, dst, perm

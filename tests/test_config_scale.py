@@ -176,14 +176,16 @@ def test_c1_sharded_aucroc_parity_with_reference(cuda):
 
 
 # -- row-block (chunked) graph construction: the C5 path -----------------------------
+@pytest.mark.parametrize("keep", [False, True])
 @pytest.mark.parametrize("dens", [False, True])
-def test_blocked_rmat_csr_equals_one_shot(cuda, dens):
-    """The row-block CSR build (bounded key scratch, samples regenerated per
-    block) equals the one-shot build bit for bit."""
+def test_blocked_rmat_csr_equals_one_shot(cuda, dens, keep):
+    """The row-block CSR build (bounded key scratch; samples regenerated per
+    block, or generated once and kept) equals the one-shot build bit for
+    bit."""
     a = gb.rmat_graph(16, 1 << 20, 3, densify_ids=dens)
     for cap, batch in [(1 << 18, 1 << 18), (50_000, 300_000)]:
         b = gb.rmat_graph(16, 1 << 20, 3, densify_ids=dens, max_block_keys=cap,
-                          batch_samples=batch)
+                          batch_samples=batch, keep_samples=keep)
         assert (a.num_vertices, a.num_edges) == (b.num_vertices, b.num_edges)
         assert np.array_equal(a.xadj, b.xadj) and np.array_equal(a.adj, b.adj)
 
