@@ -116,14 +116,20 @@ def pair_index(K: int) -> dict[tuple[int, int], int]:
     return {pr: i for i, pr in enumerate(rotation_pairs(K))}
 
 
-def round_lr(lr0: float, rot: int, ri: int, rotations: int, K: int) -> float:
-    """Learning rate of round ri of rotation rot: lr_at (trainer.py:179-181)
-    over rotations * K rounds, i.e. decaying within a rotation as the
-    in-memory pass decays within a level's epochs.  (train_large decays per
-    rotation, bigtrain.py:432; with the one or two rotations that CLI-default
-    budgets give a level, that keeps lr near lr0 for the whole level and the
-    sharded AUCROC drifts well above the in-memory path's.)"""
-    return lr_at(lr0, rot * K + ri, rotations * K)
+def round_lr(lr0: float, rot: int, ri: int, rotations: int, K: int, epochs: int) -> float:
+    """Learning rate of round ri of rotation rot of a level trained for
+    `epochs` epochs: the in-memory rate of the epoch that round's share of
+    the level's work falls in, lr_at(lr0, j, epochs) with
+    j = floor((rot * K + ri) * epochs / (rotations * K)) (trainer.py:179-181,
+    one rate per epoch, edge-scaled epochs being ceil(E/V) passes at one
+    rate).  (train_large decays per rotation, bigtrain.py:432; with the one
+    or two rotations that CLI-default budgets give a level, that keeps lr
+    near lr0 for the whole level and the sharded AUCROC drifts well above the
+    in-memory path's.  Decaying per round regardless of epochs instead halved
+    the mean rate of a one-epoch edge-scaled level, whose in-memory passes
+    all run at lr0.)"""
+    j = ((rot * K + ri) * epochs) // max(rotations * K, 1)
+    return lr_at(lr0, j, max(epochs, 1))
 
 
 def pair_rounds(K: int) -> dict[tuple[int, int], int]:
@@ -647,7 +653,7 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
             seeds = np.array([_lib.u64(_derived_seed(cfg.seed, rng_stream, rot * P + q))
                               for q in range(P)], dtype=np.uint64)
             h[:, 0] = seeds.view(np.int64)
-            h[:, 1] = np.array([round_lr(cfg.learning_rate, rot, rnd_of[pr], rotations, K)
+            h[:, 1] = np.array([round_lr(cfg.learning_rate, rot, rnd_of[pr], rotations, K, e_i)
                                 for pr in pairs_by_index], dtype=np.float64).view(np.int64)
             ptab.copy_(hbuf[k], non_blocking=True)
             ev = torch.cuda.Event()
@@ -670,7 +676,7 @@ def train_tournament_parts(g: Graph, store: PartStore, cfg: TrainConfig, e_i: in
                 seed = _derived_seed(cfg.seed, rng_stream, rot * P + index[(a, b)])
                 prm = ptab.data_ptr() + 16 * index[(a, b)] if ptab is not None else None
                 lst.append((k, PairStep(a, b, lo_a, hi_a, lo_b, hi_b, seed,
-                                        round_lr(cfg.learning_rate, rot, ri, rotations, K),
+                                        round_lr(cfg.learning_rate, rot, ri, rotations, K, e_i),
                                         prm)))
             out.append((r, lst))
         return out
@@ -973,14 +979,14 @@ def train_multilevel_sharded(g0: Graph, cfg: TrainConfig, threshold: int = 100,
     """train_multilevel (trainer.py:252-288) with the finest `shard_levels`
     levels trained by the tournament across ranks.
 
-    shard_levels=1 (default): the finest level only.  With the rotation lr
-    decaying per round (round_lr) it stays closest to the in-memory ladder's
-    AUCROC across the measured schedules (8 ranks; C3 vertex-pass +0.005,
-    C3 edge-scaled -0.002, friendster shape vertex-pass -0.007; C1 over 30
-    paired seeds +0.002 / +0.005 at 2 / 4 ranks); 2 / 3 levels project 2.5x /
-    3.9x instead of 1.4x on 8 GPUs for C3 edge-scaled but drift further
-    (profiles/r02_c3_shard_levels_round_decay.jsonl,
-    r02_c1_sharded_aucroc_round_decay.jsonl, r02_c4_sharded_round_decay.jsonl).
+    shard_levels=1 (default): the finest level only.  With each round at the
+    in-memory rate of its epoch (round_lr) it stays closest to the in-memory
+    ladder's AUCROC across the measured schedules (8 ranks; C3 vertex-pass
+    +0.007, C3 edge-scaled -0.001, friendster shape vertex-pass -0.009; C1
+    over 30 paired seeds +0.001 / +0.003 at 2 / 4 ranks); 2 / 3 levels
+    project 2.5x / 3.9x instead of 1.4x on 8 GPUs for C3 edge-scaled but
+    drift further (profiles/r02_sharded_epoch_lr.jsonl,
+    r02_c3_shard_levels_round_decay.jsonl).
 
     Every rank coarsens (the device collapse is deterministic, so the
     hierarchies are identical with no communication).  Levels above the

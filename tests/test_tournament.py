@@ -88,7 +88,7 @@ def _sequential_replay(orc, g, x, a, M, cfg, e_i, G, B=5, stream=0):
     P = len(idx)
     rnd_of = tn.pair_rounds(K)
     for r, (pa, pb) in tn.sequential_order(K, rot):
-        lr = tn.round_lr(cfg.learning_rate, r, rnd_of[(pa, pb)], rot, K)
+        lr = tn.round_lr(cfg.learning_rate, r, rnd_of[(pa, pb)], rot, K, e_i)
         seed = gb.bigtrain._derived_seed(cfg.seed, stream, r * P + idx[(pa, pb)])
         la, ha, lb, hb = int(bnd[pa]), int(bnd[pa + 1]), int(bnd[pb]), int(bnd[pb + 1])
         A = M[la:ha]
@@ -500,3 +500,20 @@ def test_gloo_processes_on_one_gpu_sharded_multilevel(cuda, orc):
         ref, _ = gb.train_multilevel_sharded(g, cfg, num_ranks=2, shard_levels=2)
         for r in range(2):
             assert np.array_equal(np.load(f"{out}.{r}.npy"), ref), r
+
+
+def test_round_lr_follows_the_in_memory_epochs():
+    """round_lr gives each round the in-memory rate of the epoch its share of
+    the level's work falls in: a one-epoch level (edge-scaled: ceil(E/V)
+    passes at one rate) trains every round at lr0; a level with one epoch
+    per round decays per round; the rate never increases."""
+    lr0, K = 0.035, 8
+    for rotations in (1, 3):
+        R = rotations * K
+        one = [tn.round_lr(lr0, r // K, r % K, rotations, K, 1) for r in range(R)]
+        assert all(x == lr0 for x in one)
+        per_round = [tn.round_lr(lr0, r // K, r % K, rotations, K, R) for r in range(R)]
+        assert per_round == [gb.lr_at(lr0, r, R) for r in range(R)]
+        for e in (2, 5, 83, 1000):
+            seq = [tn.round_lr(lr0, r // K, r % K, rotations, K, e) for r in range(R)]
+            assert all(a >= b for a, b in zip(seq, seq[1:])) and seq[0] == lr0
