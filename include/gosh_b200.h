@@ -109,10 +109,15 @@ int gb_mapped_keys_range(const int64_t *xadj, const int32_t *adj, int64_t num_ve
  * (int64[c1 - c0]) holds row c0 + r's start in keys on entry (an exclusive
  * scan of gb_mapped_histogram over the block) and its end on return.  Same
  * keys, spread over per-row atomics; replaces the single-cursor form in
- * build_coarse_graph's blocks (reference coarsen.py:256-281). */
+ * build_coarse_graph's blocks (reference coarsen.py:256-281).  heavy
+ * (int64[1 + heavy_cap], or NULL with heavy_cap 0) queues the vertices of
+ * more than heavy_arcs (>= 32) arcs, whose arcs are then split over all
+ * warps; a full queue falls back to one warp per vertex (heavy_cap >=
+ * E / heavy_arcs never fills). */
 int gb_mapped_keys_rows(const int64_t *xadj, const int32_t *adj, int64_t num_vertices,
                         const int32_t *cmap, int64_t num_clusters, int64_t c0, int64_t c1,
-                        int64_t *row_cursor, uint64_t *keys, void *stream_handle);
+                        int64_t *row_cursor, uint64_t *keys, int64_t *heavy,
+                        int64_t heavy_cap, int64_t heavy_arcs, void *stream_handle);
 int gb_keys_to_rows_workspace(int64_t num_keys, int64_t rows, int64_t num_cols,
                               size_t *bytes);
 int gb_keys_to_rows(uint64_t *keys, int64_t num_keys, int64_t rows, int64_t num_cols,

@@ -60,7 +60,8 @@ SIGNATURES = {
     "gb_arc_keys_range": (_int, [_p, _p, _i64, C.c_uint, _i64, _i64, _i64, _p, _p, _p]),
     "gb_mapped_histogram": (_int, [_p, _p, _i64, _p, _p, _p]),
     "gb_mapped_keys_range": (_int, [_p, _p, _i64, _p, _i64, _i64, _i64, _p, _p, _p]),
-    "gb_mapped_keys_rows": (_int, [_p, _p, _i64, _p, _i64, _i64, _i64, _p, _p, _p]),
+    "gb_mapped_keys_rows": (_int, [_p, _p, _i64, _p, _i64, _i64, _i64, _p, _p, _p, _i64, _i64,
+                                   _p]),
     "gb_keys_to_rows_workspace": (_int, [_i64, _i64, _i64, _psz]),
     "gb_keys_to_rows": (_int, [_p, _i64, _i64, _i64, _i64, _p, _p, _pi64, _p, _sz, _p]),
     "gb_rmat_edges_range": (_int, [_int, _i64, _i64, _dbl, _dbl, _dbl, _u64, _p, _p, _p, _p]),

@@ -13,6 +13,7 @@ access.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -181,6 +182,9 @@ def collapse_map_parallel(g: Graph, order, num_workers: int,
     return collapse_map(g, order)
 
 
+HEAVY_ARCS = 8192  # row-block builds split vertices above this over all warps
+
+
 def build_coarse_graph(g: Graph, m: Mapping, num_workers: int = 1,
                        max_block_keys: int | None = None, scratch: dict | None = None) -> Graph:
     """Contract g along m: clusters become vertices, parallel arcs merged,
@@ -200,13 +204,18 @@ def build_coarse_graph(g: Graph, m: Mapping, num_workers: int = 1,
                   _lib.ptr(hist), st)
 
         starts = torch.cumsum(hist, 0) - hist  # each row's first key (exclusive scan)
+        # hubs (> HEAVY_ARCS arcs) are split over all warps; at most E / HEAVY_ARCS
+        heavy_arcs = int(os.environ.get("GB_HEAVY_ARCS", str(HEAVY_ARCS)))
+        heavy_cap = E // heavy_arcs + 1
+        heavy = torch.empty(heavy_cap + 1, dtype=torch.int64, device="cuda")
 
         def fill(c0, c1, keys, cursor):
             # per-row cursors (gb_mapped_keys_rows): the block's rows start at
             # their scanned offsets, so the appends spread over the rows
             row_cursor = starts[c0:c1] - starts[c0]
             _lib.call("gb_mapped_keys_rows", _lib.ptr(xadj), _lib.ptr(adj), V, _lib.ptr(cmap),
-                      nc, c0, c1, _lib.ptr(row_cursor), _lib.ptr(keys), st)
+                      nc, c0, c1, _lib.ptr(row_cursor), _lib.ptr(keys), _lib.ptr(heavy),
+                      heavy_cap, heavy_arcs, st)
             cursor.copy_(hist[c0:c1].sum().reshape(1))
 
         return csr_from_blocks(nc, nc, hist, fill, max_block_keys, directed=g.directed,

@@ -987,11 +987,42 @@ __global__ void mapped_keys_range_kernel(const int64_t *__restrict__ xadj,
 // them over the block's rows.  Each warp tests the clusters of 32 of its
 // vertices at once (warp w owns vertices w, w + nwarps, ...: the hubs, which
 // lead the rank-ordered ids of a coarse level, stay spread over the warps).
+// the contracted arcs e0..e1 of a vertex of cluster cv, appended by one warp
+__device__ __forceinline__ void append_mapped_arcs(const int32_t *__restrict__ adj,
+                                                   const int32_t *__restrict__ cmap,
+                                                   int64_t e0, int64_t e1, int64_t cv,
+                                                   int64_t c0, uint64_t nc,
+                                                   uint64_t *__restrict__ keys,
+                                                   unsigned long long *__restrict__ row_cursor,
+                                                   int lane, unsigned lt) {
+  for (int64_t eb = e0; eb < e1; eb += 32) {
+    const int64_t e = eb + lane;
+    int64_t cu = cv;
+    if (e < e1) cu = cmap[adj[e]];
+    const bool emit = cu != cv;
+    const unsigned m = __ballot_sync(0xffffffffu, emit);
+    if (!m) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(row_cursor + (cv - c0), (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (emit) keys[base + __popc(m & lt)] = (uint64_t)(cv - c0) * nc + (uint64_t)cu;
+  }
+}
+
+// Vertices with more than heavy_arcs arcs (the hubs of a coarse level: one
+// warp walking a 10M-arc hub held a whole block's launch for ~130 ms at C5)
+// are queued instead and split into kHeavyPieces pieces for all warps
+// (mapped_keys_rows_heavy_kernel); a full queue falls back to the warp.
+constexpr int64_t kHeavyPieces = 64;
+
 __global__ void mapped_keys_rows_kernel(const int64_t *__restrict__ xadj,
                                         const int32_t *__restrict__ adj,
                                         const int32_t *__restrict__ cmap, int64_t V, int64_t c0,
                                         int64_t c1, uint64_t nc, uint64_t *__restrict__ keys,
-                                        unsigned long long *__restrict__ row_cursor) {
+                                        unsigned long long *__restrict__ row_cursor,
+                                        int64_t *__restrict__ heavy, int64_t heavy_cap,
+                                        int64_t heavy_arcs,
+                                        unsigned long long *__restrict__ heavy_count) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1006,19 +1037,40 @@ __global__ void mapped_keys_rows_kernel(const int64_t *__restrict__ xadj,
       const int64_t v = vb + (int64_t)src_lane * nwarps;
       const int64_t cv = __shfl_sync(0xffffffffu, cl, src_lane);
       const int64_t e0 = xadj[v], e1 = xadj[v + 1];
-      for (int64_t eb = e0; eb < e1; eb += 32) {
-        const int64_t e = eb + lane;
-        int64_t cu = cv;
-        if (e < e1) cu = cmap[adj[e]];
-        const bool emit = cu != cv;
-        const unsigned m = __ballot_sync(0xffffffffu, emit);
-        if (!m) continue;
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(row_cursor + (cv - c0), (unsigned long long)__popc(m));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (emit) keys[base + __popc(m & lt)] = (uint64_t)(cv - c0) * nc + (uint64_t)cu;
+      if (heavy_cap > 0 && e1 - e0 > heavy_arcs) {
+        unsigned long long slot = 0;
+        if (lane == 0) slot = atomicAdd(heavy_count, 1ull);
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if ((int64_t)slot < heavy_cap) {
+          if (lane == 0) heavy[slot] = v;
+          continue;
+        }
       }
+      append_mapped_arcs(adj, cmap, e0, e1, cv, c0, nc, keys, row_cursor, lane, lt);
     }
+  }
+}
+
+__global__ void mapped_keys_rows_heavy_kernel(const int64_t *__restrict__ xadj,
+                                              const int32_t *__restrict__ adj,
+                                              const int32_t *__restrict__ cmap, int64_t c0,
+                                              uint64_t nc, uint64_t *__restrict__ keys,
+                                              unsigned long long *__restrict__ row_cursor,
+                                              const int64_t *__restrict__ heavy,
+                                              int64_t heavy_cap,
+                                              const unsigned long long *__restrict__ heavy_count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned lt = lanemask_lt();
+  const int64_t queued = (int64_t)*heavy_count, n = queued < heavy_cap ? queued : heavy_cap;
+  for (int64_t item = warp; item < n * kHeavyPieces; item += nwarps) {
+    const int64_t v = heavy[item / kHeavyPieces], piece = item % kHeavyPieces;
+    const int64_t e0 = xadj[v], e1 = xadj[v + 1];
+    const int64_t len = ((e1 - e0 + kHeavyPieces - 1) / kHeavyPieces + 31) & ~int64_t(31);
+    const int64_t a = e0 + piece * len, b = e1 < a + len ? e1 : a + len;
+    if (a >= b) continue;
+    append_mapped_arcs(adj, cmap, a, b, (int64_t)cmap[v], c0, nc, keys, row_cursor, lane, lt);
   }
 }
 
@@ -1094,17 +1146,30 @@ GB_API int gb_mapped_keys_range(const int64_t *xadj, const int32_t *adj, int64_t
 GB_API int gb_mapped_keys_rows(const int64_t *xadj, const int32_t *adj, int64_t num_vertices,
                                const int32_t *cmap, int64_t num_clusters, int64_t c0,
                                int64_t c1, int64_t *row_cursor, uint64_t *keys,
+                               int64_t *heavy, int64_t heavy_cap, int64_t heavy_arcs,
                                void *stream_handle) {
   GB_REQUIRE(num_vertices >= 1 && xadj && cmap && keys && row_cursor && c0 >= 0 && c1 >= c0 &&
-                 c1 <= num_clusters,
+                 c1 <= num_clusters && heavy_cap >= 0 && (heavy_cap == 0 || heavy) &&
+                 heavy_arcs >= 32,
              "gb_mapped_keys_rows: bad args");
   if (c1 == c0) return GB_OK;
+  cudaStream_t st = as_stream(stream_handle);
+  // heavy[0] counts the queue, heavy[1..heavy_cap] holds it
+  unsigned long long *count = reinterpret_cast<unsigned long long *>(heavy);
+  if (heavy_cap > 0) GB_CUDA_TRY(cudaMemsetAsync(heavy, 0, sizeof(int64_t), st));
   const int blocks =
       (int)std::min<int64_t>((num_vertices + 255) / 256, (int64_t)num_sms() * 16);
-  mapped_keys_rows_kernel<<<std::max(blocks, 1), 256, 0, as_stream(stream_handle)>>>(
+  mapped_keys_rows_kernel<<<std::max(blocks, 1), 256, 0, st>>>(
       xadj, adj, cmap, num_vertices, c0, c1, (uint64_t)num_clusters, keys,
-      reinterpret_cast<unsigned long long *>(row_cursor));
+      reinterpret_cast<unsigned long long *>(row_cursor), heavy_cap ? heavy + 1 : nullptr,
+      heavy_cap, heavy_arcs, count);
   GB_CHECK_LAUNCH();
+  if (heavy_cap > 0) {
+    mapped_keys_rows_heavy_kernel<<<num_sms() * 8, 256, 0, st>>>(
+        xadj, adj, cmap, c0, (uint64_t)num_clusters, keys,
+        reinterpret_cast<unsigned long long *>(row_cursor), heavy + 1, heavy_cap, count);
+    GB_CHECK_LAUNCH();
+  }
   return GB_OK;
 }
 

@@ -210,11 +210,14 @@ def test_blocked_arc_batches_equal_from_edges(cuda):
     assert np.array_equal(got.xadj, ref.xadj) and np.array_equal(got.adj, ref.adj)
 
 
+@pytest.mark.parametrize("heavy_arcs", [8192, 32])
 @pytest.mark.parametrize("cap", [100_000, 3_000])
-def test_blocked_coarsening_equals_one_shot(cuda, orc, cap):
+def test_blocked_coarsening_equals_one_shot(cuda, orc, cap, heavy_arcs, monkeypatch):
     """Row blocks (per-row key cursors, gb_mapped_keys_rows) build the same
     hierarchy as the one-shot coarse CSR; cap 3,000 puts hub rows above the
-    cap in blocks of their own."""
+    cap in blocks of their own; heavy_arcs 32 sends most vertices through
+    the split-hub path."""
+    monkeypatch.setenv("GB_HEAVY_ARCS", str(heavy_arcs))
     g = gb.rmat_graph(16, 1 << 20, 5, densify_ids=True)
     h1 = gb.coarsen_all(g, threshold=100)
     h2 = gb.coarsen_all(g, threshold=100, max_block_keys=cap)
