@@ -220,7 +220,14 @@ def build_coarse_graph(g: Graph, m: Mapping, num_workers: int = 1,
 
         return csr_from_blocks(nc, nc, hist, fill, max_block_keys, directed=g.directed,
                                scratch=scratch)
-    ws, wsb = _lib.workspace("gb_coarse_csr_workspace", V, E, nc)
+    n_ws = C.c_size_t(0)
+    _lib.call("gb_coarse_csr_workspace", V, E, nc, C.byref(n_ws))
+    wsb = int(n_ws.value)
+    if scratch is not None:  # coarsen_all: the level-0 workspace serves every level
+        from .graph import _scratch_buffer
+        ws = _scratch_buffer(scratch, "coarse_ws", max(wsb, 1), torch.uint8)
+    else:
+        ws, wsb = _lib.workspace("gb_coarse_csr_workspace", V, E, nc)
     x2 = torch.empty(nc + 1, dtype=torch.int64, device="cuda")
     a2 = torch.empty(max(E, 1), dtype=torch.int32, device="cuda")
     ne = C.c_int64(0)

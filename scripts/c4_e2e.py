@@ -1,0 +1,85 @@
+"""The north star's metric at its target shape on ONE GPU: embed wall-time
+of the friendster-shaped R-MAT (scale 27, 1.9B samples -> 61.1M vertices,
+3.74G arcs) through the public call a user makes, train_multilevel(host
+Graph) -> numpy matrix, with the CLI's large-graph defaults (d=128, 200
+vertex-pass epochs) -- CSR upload, coarsening, every level's training and
+the 31 GB download inside the clock.  The graph is built on the device and
+brought to host numpy arrays first (the user's input).  REPS repeats."""
+import json
+import os
+import sys
+import time
+
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "backend:cudaMallocAsync")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_2008_12336_b200 as gb  # noqa: E402
+
+SCALE = int(os.environ.get("SCALE", "27"))
+SAMPLES = int(os.environ.get("SAMPLES", "1900000000"))
+EPOCHS = int(os.environ.get("EPOCHS", "200"))
+UNIT = os.environ.get("UNIT", "vertex-pass")
+REPS = int(os.environ.get("REPS", "2"))
+
+
+def main():
+    t0 = time.perf_counter()
+    g = gb.rmat_graph(SCALE, SAMPLES, 7, densify_ids=True)
+    xh, ah = g.xadj, g.adj  # host copies: the user's graph
+    V, E = g.num_vertices, g.num_edges
+    del g
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    print(json.dumps({"phase": "input", "vertices": V, "arcs": E,
+                      "host_bytes": int(xh.nbytes + ah.nbytes),
+                      "s": time.perf_counter() - t0}), flush=True)
+    cfg = gb.TrainConfig(dim=128, total_epochs=EPOCHS, smoothing_ratio=0.3, learning_rate=0.035,
+                         negative_samples=3, seed=1, epoch_unit=UNIT)
+    for rep in range(REPS):
+        host_graph = gb.Graph(V, E, xadj=xh, adj=ah)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        M = gb.train_multilevel(host_graph, cfg)
+        s = time.perf_counter() - t0
+        print(json.dumps({"phase": "train_multilevel", "rep": rep, "unit": UNIT, "epochs": EPOCHS,
+                          "embed_s": s, "matrix_bytes": int(M.nbytes),
+                          "finite": bool(float(abs(M[:1000]).max()) < 1e30),
+                          "peak_gib": round(torch.cuda.max_memory_allocated() / 2**30, 2)}),
+              flush=True)
+        del M, host_graph
+        torch.cuda.empty_cache()
+    # the same calls with synchronised phase clocks (where the time goes)
+    from paper_2008_12336_b200._staging import device_to_numpy
+    ph, t = {}, time.perf_counter()
+
+    def mark(name, t):
+        torch.cuda.synchronize()
+        now = time.perf_counter()
+        ph[name] = ph.get(name, 0.0) + now - t
+        return now
+    t0 = t
+    fresh = gb.Graph(V, E, xadj=xh, adj=ah)
+    fresh.device_csr()
+    t = mark("csr_upload", t)
+    h = gb.coarsen_all(fresh, threshold=100)
+    t = mark("coarsen", t)
+    plan = gb.epoch_plan(cfg.total_epochs, cfg.smoothing_ratio, h.depth).per_level
+    M = torch.from_numpy(gb.init_embedding(h.graphs[-1].num_vertices, cfg.dim, cfg.seed)).cuda()
+    for i in range(h.depth - 1, -1, -1):
+        if plan[i] > 0:
+            gb.train_level(h.graphs[i], M, cfg, int(plan[i]), rng_stream=i)
+        t = mark("train", t)
+        if i > 0:
+            M = gb.expand_embedding(M, h.mappings[i - 1])
+            t = mark("expand", t)
+    out = device_to_numpy(M)
+    t = mark("download", t)
+    ph["total"] = time.perf_counter() - t0
+    print(json.dumps({"phase": "phases", "phases_s": {k: round(v, 3) for k, v in ph.items()},
+                      "download_gbs": out.nbytes / ph["download"] / 1e9}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
