@@ -11,7 +11,10 @@ import os
 import sys
 import time
 
-os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "backend:cudaMallocAsync")
+# native caching allocator with large blocks never split: fresh tens-of-GiB
+# allocations get their own segments (no fragmentation for the 116 GB matrix,
+# no on-the-spot pool mapping as under cudaMallocAsync; DESIGN 5b)
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "max_split_size_mb:1024")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
