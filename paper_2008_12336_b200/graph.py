@@ -250,13 +250,22 @@ def _scratch_buffer(scratch: dict | None, name: str, numel: int, dtype) -> torch
     """A device buffer of at least numel elements, kept in `scratch` between
     row-block builds (a coarsening ladder asks for the same tens of GiB at
     every level; re-allocating them cost 0.2-1.1 s per level at C5)."""
+    def alloc():
+        try:
+            return torch.empty(numel, dtype=dtype, device="cuda")
+        except torch.OutOfMemoryError:
+            # tens of GiB can fail on cached-but-fragmented blocks: hand them
+            # back to the driver and retry once (as _lib.workspace does)
+            torch.cuda.empty_cache()
+            return torch.empty(numel, dtype=dtype, device="cuda")
+
     if scratch is None:
-        return torch.empty(numel, dtype=dtype, device="cuda")
+        return alloc()
     buf = scratch.get(name)
     if buf is None or buf.numel() < numel:
         scratch.pop(name, None)
         del buf
-        buf = torch.empty(numel, dtype=dtype, device="cuda")
+        buf = alloc()
         scratch[name] = buf
     return buf[:numel]
 
